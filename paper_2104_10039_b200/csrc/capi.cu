@@ -1,0 +1,460 @@
+// capi.cu — the extern "C" boundary (include/ggb.h) and the program
+// dispatch. Each gg_run_* is the device counterpart of
+// gg::run<Program>(graph, program, config) (engine.hpp:141-143).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "engine.cuh"
+#include "programs.cuh"
+
+namespace ggb {
+
+// 32-aligned, edge-balanced destination ranges.
+static std::vector<uint64_t> plan_partition(uint64_t n, const uint64_t* off, int nranks) {
+    std::vector<uint64_t> b(nranks + 1, 0);
+    b[nranks] = n;
+    const uint64_t e = off[n];
+    for (int r = 1; r < nranks; ++r) {
+        const uint64_t target = (uint64_t)((long double)e * r / nranks);
+        uint64_t v = (uint64_t)(std::lower_bound(off, off + n + 1, target) - off);
+        v = (v / kWindow) * kWindow;
+        if (v < b[r - 1]) v = b[r - 1];
+        if (v > n) v = n;
+        b[r] = v;
+    }
+    return b;
+}
+
+__global__ void rebase_kernel(const uint64_t* __restrict__ in, uint64_t count, uint64_t base,
+                              uint64_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] - base;
+}
+
+static void setup_common(DevGraph& g, const gg_part_opts* opts) {
+    int dev = 0;
+    if (opts && opts->device >= 0) dev = opts->device;
+    else GGB_CUDA(cudaGetDevice(&dev));
+    int count = 0;
+    GGB_CUDA(cudaGetDeviceCount(&count));
+    if (count < 1) throw Error(GG_CUDA, "no CUDA device");
+    g.device = dev;
+    GGB_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    GGB_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+        throw Error(GG_CUDA, std::string("libggb.so needs an sm_100 device, found ") + prop.name);
+    g.num_sms = prop.multiProcessorCount;
+    GGB_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    g.rank = opts ? opts->rank : 0;
+    g.nranks = opts ? std::max(1, opts->nranks) : 1;
+    g.exchange = opts ? static_cast<gg_exchange*>(opts->exchange) : nullptr;
+    if (g.nranks > 1 && !g.exchange)
+        throw Error(GG_INVALID_ARGUMENT, "nranks > 1 needs an exchange (gg_exchange_nccl_create)");
+    if (g.rank < 0 || g.rank >= g.nranks) throw Error(GG_INVALID_ARGUMENT, "rank out of range");
+}
+
+static void finish_graph(DevGraph& g, const std::vector<uint64_t>& host_off_full) {
+    g.bounds = plan_partition(g.n, host_off_full.data(), g.nranks);
+    g.ebounds.resize(g.nranks + 1);
+    for (int r = 0; r <= g.nranks; ++r) g.ebounds[r] = host_off_full[g.bounds[r]];
+    g.v_begin = g.bounds[g.rank];
+    g.v_end = g.bounds[g.rank + 1];
+    g.nloc = g.v_end - g.v_begin;
+    g.e_base = g.ebounds[g.rank];
+    g.e_loc = g.ebounds[g.rank + 1] - g.e_base;
+    if (g.n > 0xffffffffull) throw Error(GG_INVALID_ARGUMENT, "more than 2^32-1 vertices");
+}
+
+}  // namespace ggb
+
+using namespace ggb;
+
+extern "C" {
+
+const char* gg_status_string(gg_status s) {
+    switch (s) {
+        case GG_OK: return "ok";
+        case GG_INVALID_ARGUMENT: return "invalid argument";
+        case GG_INVALID_PROPERTY: return "invalid property";
+        case GG_CUDA: return "CUDA error";
+        case GG_NCCL: return "NCCL error";
+        case GG_OOM: return "out of memory";
+        case GG_INTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+int gg_abi_version(void) { return GGB_ABI_VERSION; }
+
+gg_status gg_partition_plan(uint64_t n, const uint64_t* offsets, int nranks, uint64_t* bounds) {
+    return guarded(nullptr, [&] {
+        if (nranks < 1) throw Error(GG_INVALID_ARGUMENT, "nranks must be >= 1");
+        auto b = plan_partition(n, offsets, nranks);
+        std::copy(b.begin(), b.end(), bounds);
+    });
+}
+
+gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
+                              gg_dev_graph** out, gg_error* err) {
+    return guarded(err, [&] {
+        if (!csc || !out) throw Error(GG_INVALID_ARGUMENT, "null argument");
+        if (csc->n && !csc->offsets) throw Error(GG_INVALID_ARGUMENT, "offsets is null");
+        if (csc->offsets && csc->offsets[csc->n] != csc->e)
+            throw Error(GG_INVALID_ARGUMENT, "offsets[n] != e");
+        if (csc->e && !csc->sources) throw Error(GG_INVALID_ARGUMENT, "sources is null");
+        if (csc->weight_kind != GG_W_NONE && csc->e && !csc->weights)
+            throw Error(GG_INVALID_ARGUMENT, "weights is null");
+        auto* h = new gg_dev_graph;
+        try {
+            DevGraph& g = h->g;
+            setup_common(g, opts);
+            g.n = csc->n;
+            g.e_global = csc->e;
+            g.wkind = csc->weight_kind;
+            std::vector<uint64_t> off(csc->offsets ? csc->offsets : nullptr,
+                                      csc->offsets ? csc->offsets + csc->n + 1 : nullptr);
+            if (off.empty()) off.assign(1, 0);
+            finish_graph(g, off);
+            GGB_CUDA(cudaMalloc(&g.off, (g.nloc + 1) * 8));
+            GGB_CUDA(cudaMalloc(&g.src, (g.e_loc + 1) * 4));
+            GGB_CUDA(cudaMalloc(&g.outdeg, (g.n + 1) * 4));
+            std::vector<uint64_t> loc(g.nloc + 1);
+            for (uint64_t i = 0; i <= g.nloc; ++i) loc[i] = off[g.v_begin + i] - g.e_base;
+            GGB_CUDA(cudaMemcpyAsync(g.off, loc.data(), (g.nloc + 1) * 8, cudaMemcpyHostToDevice,
+                                     g.stream));
+            if (g.e_loc)
+                GGB_CUDA(cudaMemcpyAsync(g.src, csc->sources + g.e_base, g.e_loc * 4,
+                                         cudaMemcpyHostToDevice, g.stream));
+            const size_t wb = weight_size(g.wkind);
+            if (wb) {
+                GGB_CUDA(cudaMalloc(&g.w, (g.e_loc + 1) * wb));
+                if (g.e_loc)
+                    GGB_CUDA(cudaMemcpyAsync(g.w, static_cast<const char*>(csc->weights) + g.e_base * wb,
+                                             g.e_loc * wb, cudaMemcpyHostToDevice, g.stream));
+            }
+            if (csc->out_degree) {
+                if (g.n)
+                    GGB_CUDA(cudaMemcpyAsync(g.outdeg, csc->out_degree, g.n * 4,
+                                             cudaMemcpyHostToDevice, g.stream));
+            } else {
+                std::vector<uint32_t> deg(g.n, 0);
+                for (uint64_t i = 0; i < csc->e; ++i) {
+                    if (csc->sources[i] >= g.n)
+                        throw Error(GG_INVALID_ARGUMENT, "edge source out of range");
+                    ++deg[csc->sources[i]];
+                }
+                if (g.n)
+                    GGB_CUDA(cudaMemcpyAsync(g.outdeg, deg.data(), g.n * 4, cudaMemcpyHostToDevice,
+                                             g.stream));
+                GGB_CUDA(cudaStreamSynchronize(g.stream));
+            }
+            build_tasks(g, g.off, "full", g.full);
+            GGB_CUDA(cudaStreamSynchronize(g.stream));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* opts,
+                                   gg_dev_graph** out, gg_error* err) {
+    return guarded(err, [&] {
+        if (!p || !out) throw Error(GG_INVALID_ARGUMENT, "null argument");
+        auto* h = new gg_dev_graph;
+        try {
+            DevGraph& g = h->g;
+            setup_common(g, opts);
+            RmatCsc r = rmat_generate(*p, g.stream);
+            g.n = r.n;
+            g.e_global = r.e;
+            g.wkind = p->weight_kind;
+            std::vector<uint64_t> off(r.n + 1);
+            GGB_CUDA(cudaMemcpy(off.data(), r.off, (r.n + 1) * 8, cudaMemcpyDeviceToHost));
+            finish_graph(g, off);
+            g.outdeg = r.outdeg;
+            if (g.nranks == 1) {
+                g.off = r.off;
+                g.src = r.src;
+                g.w = r.w;
+            } else {
+                GGB_CUDA(cudaMalloc(&g.off, (g.nloc + 1) * 8));
+                rebase_kernel<<<256, 256, 0, g.stream>>>(r.off + g.v_begin, g.nloc + 1, g.e_base,
+                                                          g.off);
+                GGB_CUDA(cudaGetLastError());
+                GGB_CUDA(cudaMalloc(&g.src, (g.e_loc + 1) * 4));
+                GGB_CUDA(cudaMemcpyAsync(g.src, r.src + g.e_base, g.e_loc * 4,
+                                         cudaMemcpyDeviceToDevice, g.stream));
+                const size_t wb = weight_size(g.wkind);
+                if (wb) {
+                    GGB_CUDA(cudaMalloc(&g.w, (g.e_loc + 1) * wb));
+                    GGB_CUDA(cudaMemcpyAsync(g.w, static_cast<char*>(r.w) + g.e_base * wb,
+                                             g.e_loc * wb, cudaMemcpyDeviceToDevice, g.stream));
+                }
+                GGB_CUDA(cudaStreamSynchronize(g.stream));
+                cudaFree(r.off);
+                cudaFree(r.src);
+                if (r.w) cudaFree(r.w);
+            }
+            build_tasks(g, g.off, "full", g.full);
+            GGB_CUDA(cudaStreamSynchronize(g.stream));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+gg_status gg_dev_graph_destroy(gg_dev_graph* g) {
+    return guarded(nullptr, [&] {
+        if (g) {
+            cudaSetDevice(g->g.device);
+            delete g;
+        }
+    });
+}
+
+gg_status gg_dev_graph_info(const gg_dev_graph* h, uint64_t* n, uint64_t* e, uint64_t* vb,
+                            uint64_t* ve, uint64_t* el) {
+    return guarded(nullptr, [&] {
+        if (!h) throw Error(GG_INVALID_ARGUMENT, "null graph");
+        const DevGraph& g = h->g;
+        if (n) *n = g.n;
+        if (e) *e = g.e_global;
+        if (vb) *vb = g.v_begin;
+        if (ve) *ve = g.v_end;
+        if (el) *el = g.e_loc;
+    });
+}
+
+gg_status gg_dev_graph_export(const gg_dev_graph* h, uint64_t* offsets, uint32_t* sources,
+                              void* weights, uint32_t* out_degree) {
+    return guarded(nullptr, [&] {
+        if (!h) throw Error(GG_INVALID_ARGUMENT, "null graph");
+        const DevGraph& g = h->g;
+        if (g.nranks != 1) throw Error(GG_INVALID_ARGUMENT, "export needs a single-rank graph");
+        GGB_CUDA(cudaSetDevice(g.device));
+        if (offsets) GGB_CUDA(cudaMemcpy(offsets, g.off, (g.nloc + 1) * 8, cudaMemcpyDeviceToHost));
+        if (sources && g.e_loc)
+            GGB_CUDA(cudaMemcpy(sources, g.src, g.e_loc * 4, cudaMemcpyDeviceToHost));
+        const size_t wb = weight_size(g.wkind);
+        if (weights && wb && g.e_loc)
+            GGB_CUDA(cudaMemcpy(weights, g.w, g.e_loc * wb, cudaMemcpyDeviceToHost));
+        if (out_degree && g.n)
+            GGB_CUDA(cudaMemcpy(out_degree, g.outdeg, g.n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+gg_status gg_bp_priors(uint64_t n, uint64_t seed, float* out) {
+    return guarded(nullptr, [&] {
+        float* d = nullptr;
+        GGB_CUDA(cudaMalloc(&d, (2 * n + 2) * 4));
+        bp_priors_device(n, seed, d, 0);
+        GGB_CUDA(cudaMemcpy(out, d, 2 * n * 4, cudaMemcpyDeviceToHost));
+        GGB_CUDA(cudaFree(d));
+    });
+}
+
+gg_status gg_validate(const gg_engine_config* cfg, gg_error* err) {
+    return guarded(err, [&] { validate(*cfg); });
+}
+
+int32_t gg_mode_for(int32_t scheme, uint64_t t, uint64_t alpha) { return mode_for(scheme, t, alpha); }
+
+uint64_t gg_select_superstep_iterations(uint64_t alpha, uint64_t max_it, int32_t scheme,
+                                        uint64_t* out, uint64_t cap) {
+    uint64_t k = 0;  // engine.cpp:77-90
+    if (alpha < 1) return 0;
+    if (scheme == GG_SCHEME_GG) {
+        for (uint64_t t = alpha + 1; t <= max_it; t += alpha + 1) {
+            if (k < cap && out) out[k] = t;
+            ++k;
+        }
+    } else if (scheme == GG_SCHEME_SMS && alpha + 1 <= max_it) {
+        if (k < cap && out) out[k] = alpha + 1;
+        ++k;
+    }
+    return k;
+}
+
+gg_status gg_sparsify(uint64_t e, double sigma, uint64_t seed, uint32_t* out_bitmap, gg_error* err) {
+    return guarded(err, [&] {
+        if (!(sigma >= 0.0 && sigma <= 1.0)) throw Error(GG_INVALID_ARGUMENT, "sigma must be in [0,1]");
+        DevGraph g;
+        setup_common(g, nullptr);
+        g.e_loc = e;
+        const uint64_t nwords = (e + 31) / 32;
+        uint32_t* bm = g.ws.get<uint32_t>("bm", nwords + 1);
+        sparsify_bitmap(g, bm, sigma, seed, false);
+        GGB_CUDA(cudaMemcpyAsync(out_bitmap, bm, nwords * 4, cudaMemcpyDeviceToHost, g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+    });
+}
+
+// ---- runs -----------------------------------------------------------------
+static RunIO make_io(const gg_engine_config* cfg, gg_iter_record* recs, uint64_t cap,
+                     gg_run_summary* sum, const gg_run_opts* opts, void* props, int S) {
+    RunIO io;
+    io.cfg = cfg; io.recs = recs; io.rec_cap = cap; io.sum = sum; io.opts = opts;
+    io.out_props = props; io.out_states = S;
+    if (sum) std::memset(sum, 0, sizeof(*sum));
+    return io;
+}
+
+static void check_run(gg_dev_graph* h, const gg_engine_config* cfg) {
+    if (!h || !cfg) throw Error(GG_INVALID_ARGUMENT, "null argument");
+    validate(*cfg);  // engine.hpp:145
+}
+
+gg_status gg_run_pr(gg_dev_graph* h, const gg_engine_config* cfg, const gg_pr_params* p,
+                    double* out_props, gg_iter_record* recs, uint64_t cap, gg_run_summary* sum,
+                    const gg_run_opts* opts, gg_error* err) {
+    return guarded(err, [&] {
+        check_run(h, cfg);
+        RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, 1);
+        if (h->g.n == 0) return;  // engine.hpp:149
+        PageRank prog;
+        prog.damping = p ? p->damping : 0.85;
+        prog.epsilon = p ? p->epsilon : 1e-7;
+        Engine<PageRank, void>::run(h->g, prog, io);  // PR ignores edge weights
+    });
+}
+
+gg_status gg_run_sssp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_sssp_params* p,
+                      double* out_props, gg_iter_record* recs, uint64_t cap, gg_run_summary* sum,
+                      const gg_run_opts* opts, gg_error* err) {
+    return guarded(err, [&] {
+        check_run(h, cfg);
+        RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, 1);
+        if (h->g.n == 0) return;
+        const uint32_t source = p ? p->source : 0;
+        const bool graded = p ? p->graded != 0 : false;
+        if (source >= h->g.n)  // algorithms.hpp:55-57
+            throw Error(GG_INVALID_ARGUMENT, "sssp source vertex out of range");
+        DevGraph& g = h->g;
+        if (g.wkind == GG_W_NONE || g.wkind == GG_W_U32) {
+            SsspU32 prog;
+            prog.source = source;
+            prog.graded = graded;
+            if (g.wkind == GG_W_NONE) Engine<SsspU32, void>::run(g, prog, io);
+            else Engine<SsspU32, uint32_t>::run(g, prog, io);
+        } else {
+            SsspF64 prog;
+            prog.source = source;
+            prog.graded = graded;
+            if (g.wkind == GG_W_F32) Engine<SsspF64, float>::run(g, prog, io);
+            else Engine<SsspF64, double>::run(g, prog, io);
+        }
+    });
+}
+
+gg_status gg_run_wcc(gg_dev_graph* h, const gg_engine_config* cfg, uint32_t* out_props,
+                     gg_iter_record* recs, uint64_t cap, gg_run_summary* sum,
+                     const gg_run_opts* opts, gg_error* err) {
+    return guarded(err, [&] {
+        check_run(h, cfg);
+        RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, 1);
+        if (h->g.n == 0) return;
+        Engine<Wcc, void>::run(h->g, Wcc{}, io);
+    });
+}
+
+gg_status gg_run_bp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_bp_params* p,
+                    double* out_props, gg_iter_record* recs, uint64_t cap, gg_run_summary* sum,
+                    const gg_run_opts* opts, gg_error* err) {
+    return guarded(err, [&] {
+        check_run(h, cfg);
+        if (!p) throw Error(GG_INVALID_ARGUMENT, "bp params are required");
+        DevGraph& g = h->g;
+        if (p->prior_table) {
+            if (p->states != 2) throw Error(GG_INVALID_ARGUMENT, "bp with a prior table needs states == 2");
+            if (g.wkind != GG_W_F32 && g.wkind != GG_W_F64)
+                throw Error(GG_INVALID_ARGUMENT, "bp with a prior table needs per-edge couplings (f32/f64 weights)");
+            RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, 2);
+            if (g.n == 0) return;
+            float2* table = g.ws.get<float2>("bp.prior", g.n);
+            GGB_CUDA(cudaMemcpyAsync(table, p->prior_table, g.n * 8, cudaMemcpyHostToDevice, g.stream));
+            BeliefPropEdge prog;
+            prog.prior_table = table;
+            prog.epsilon = p->epsilon;
+            if (g.wkind == GG_W_F32) Engine<BeliefPropEdge, float>::run(g, prog, io);
+            else Engine<BeliefPropEdge, double>::run(g, prog, io);
+            return;
+        }
+        RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, p->states);
+        if (g.n == 0) return;
+        switch (p->states) {
+            case 2: { BeliefProp<2> b; b.coupling = p->coupling; b.epsilon = p->epsilon;
+                      Engine<BeliefProp<2>, void>::run(g, b, io); break; }
+            case 3: { BeliefProp<3> b; b.coupling = p->coupling; b.epsilon = p->epsilon;
+                      Engine<BeliefProp<3>, void>::run(g, b, io); break; }
+            case 4: { BeliefProp<4> b; b.coupling = p->coupling; b.epsilon = p->epsilon;
+                      Engine<BeliefProp<4>, void>::run(g, b, io); break; }
+            default: throw Error(GG_INVALID_ARGUMENT, "bp states must be in [2,4] on device");
+        }
+    });
+}
+
+// ---- host metrics (metrics.cpp) ------------------------------------------
+gg_status gg_topk_error(const double* approx, const double* exact, uint64_t n, uint64_t k,
+                        double* err_out) {
+    return guarded(nullptr, [&] {
+        if (k < 1 || k > n) throw Error(GG_INVALID_ARGUMENT, "topk k must be in [1, N]");
+        auto topk = [&](const double* vals) {
+            std::vector<uint32_t> idx(n);
+            std::iota(idx.begin(), idx.end(), 0u);
+            std::partial_sort(idx.begin(), idx.begin() + (long)k, idx.end(),
+                              [&](uint32_t a, uint32_t b) {
+                                  if (vals[a] != vals[b]) return vals[a] > vals[b];
+                                  return a < b;
+                              });
+            idx.resize(k);
+            return idx;
+        };
+        const auto ta = topk(approx), te = topk(exact);
+        std::vector<uint8_t> in_exact(n, 0);
+        for (uint32_t v : te) in_exact[v] = 1;
+        uint64_t missing = 0;
+        for (uint32_t v : ta) missing += in_exact[v] ? 0 : 1;
+        *err_out = (double)missing / (double)k;
+    });
+}
+
+gg_status gg_relative_error(const double* approx, const double* exact, uint64_t n, double* err_out) {
+    return guarded(nullptr, [&] {
+        if (n == 0) { *err_out = 0.0; return; }
+        double s = 0.0;
+        for (uint64_t v = 0; v < n; ++v) {
+            const double a = approx[v] + 1.0, e = exact[v] + 1.0;
+            s += std::min(1.0, std::fabs(e - a) / e);
+        }
+        *err_out = s / (double)n;
+    });
+}
+
+gg_status gg_stretch_error(const double* approx, const double* exact, uint64_t n, double* err_out) {
+    return guarded(nullptr, [&] {
+        double s = 0.0;
+        uint64_t counted = 0;
+        for (uint64_t v = 0; v < n; ++v) {
+            const double e = exact[v], a = approx[v];
+            if (a < e)
+                throw Error(GG_INVALID_ARGUMENT, "stretch_error: approximate distance below exact at vertex " +
+                                                     std::to_string(v) + " (engine bug)");
+            if (std::isinf(e)) continue;
+            if (e == 0.0 && a == 0.0) continue;
+            ++counted;
+            if (std::isinf(a) || e == 0.0) { s += 1.0; continue; }
+            s += 1.0 - e / a;
+        }
+        *err_out = counted == 0 ? 0.0 : s / (double)counted;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,197 @@
+// common.cuh — shared device/host helpers for libggb.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "ggb.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libggb.so is built for sm_100a (B200) only"
+#endif
+
+namespace ggb {
+
+constexpr int kWarp = 32;
+constexpr int kWindow = 32;              // vertices per window (one per lane)
+constexpr int kRowsPerChunk = 32;        // rows of 32 edges per warp task
+constexpr int kChunkEdges = kWarp * kRowsPerChunk;
+constexpr int kBlockThreads = 256;
+constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
+
+// splitmix64 finalizer: engine.cpp:9-14 (bit-identical on host and device).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ double to_unit(uint64_t h) {
+    return (double)(h >> 11) * 0x1.0p-53;
+}
+
+// Engine error carried to the C ABI boundary.
+struct Error : std::runtime_error {
+    gg_status status;
+    uint64_t iteration = 0;
+    uint32_t vertex = 0;
+    Error(gg_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        std::snprintf(buf, sizeof(buf), "%s: %s (%s:%d)", what, cudaGetErrorString(e), file,
+                      line);
+        throw Error(e == cudaErrorMemoryAllocation ? GG_OOM : GG_CUDA, buf);
+    }
+}
+#define GGB_CUDA(x) ::ggb::cuda_check((x), #x, __FILE__, __LINE__)
+
+inline void fill_error(gg_error* err, const Error& e) {
+    if (!err) return;
+    err->iteration = e.iteration;
+    err->vertex = e.vertex;
+    std::strncpy(err->msg, e.what(), sizeof(err->msg) - 1);
+    err->msg[sizeof(err->msg) - 1] = 0;
+}
+
+// Every extern "C" entry wraps its body with this: exceptions never cross
+// the C boundary.
+template <class F>
+gg_status guarded(gg_error* err, F&& f) {
+    try {
+        f();
+        if (err) err->msg[0] = 0;
+        return GG_OK;
+    } catch (const Error& e) {
+        fill_error(err, e);
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        if (err) std::strncpy(err->msg, "host out of memory", sizeof(err->msg) - 1);
+        return GG_OOM;
+    } catch (const std::exception& e) {
+        if (err) {
+            std::strncpy(err->msg, e.what(), sizeof(err->msg) - 1);
+            err->msg[sizeof(err->msg) - 1] = 0;
+        }
+        return GG_INTERNAL;
+    }
+}
+
+// -------------------------------------------------------------------------
+// Device-side warp helpers
+// -------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ T shfl_up_any(T v, int d) {
+    static_assert(sizeof(T) % 4 == 0, "32-bit granular types only");
+    T out;
+    const int* src = reinterpret_cast<const int*>(&v);
+    int* dst = reinterpret_cast<int*>(&out);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) dst[i] = __shfl_up_sync(0xffffffffu, src[i], d);
+    return out;
+}
+template <class T>
+__device__ __forceinline__ T shfl_idx_any(T v, int lane) {
+    static_assert(sizeof(T) % 4 == 0, "32-bit granular types only");
+    T out;
+    const int* src = reinterpret_cast<const int*>(&v);
+    int* dst = reinterpret_cast<int*>(&out);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) dst[i] = __shfl_sync(0xffffffffu, src[i], lane);
+    return out;
+}
+
+// L2 eviction policies (createpolicy) for the two access streams of the
+// gather: edge arrays are read once per iteration (evict_first), the
+// per-vertex message array is re-read randomly (evict_last).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// Streaming (read-once) 32-bit load: bypass L1, evict-first in L2.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// Random message loads, kept in L2.
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_keep(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_keep(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+// Load a trivially-copyable message of 4/8/16/32 bytes with the keep policy.
+template <class M>
+__device__ __forceinline__ M ld_msg(const M* p, uint64_t pol) {
+    M out;
+    if constexpr (sizeof(M) == 4) {
+        uint32_t v = ld_keep(reinterpret_cast<const uint32_t*>(p), pol);
+        memcpy(&out, &v, 4);
+    } else if constexpr (sizeof(M) == 8) {
+        uint2 v = ld_keep(reinterpret_cast<const uint2*>(p), pol);
+        memcpy(&out, &v, 8);
+    } else if constexpr (sizeof(M) % 16 == 0) {
+        uint4 v[sizeof(M) / 16];
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(M) / 16); ++i)
+            v[i] = ld_keep(reinterpret_cast<const uint4*>(p) + i, pol);
+        memcpy(&out, v, sizeof(M));
+    } else {
+        out = *p;
+    }
+    return out;
+}
+
+// L2-coherent load of data written by other CTAs in the same kernel
+// (after their __threadfence + ticket atomic).
+template <class T>
+__device__ __forceinline__ T ld_cg_any(const T* p) {
+    static_assert(sizeof(T) % 4 == 0, "32-bit granular types only");
+    T out;
+    int* dst = reinterpret_cast<int*>(&out);
+    const int* src = reinterpret_cast<const int*>(p);
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) dst[i] = __ldcg(src + i);
+    return out;
+}
+
+template <class W>
+struct WeightIO {
+    __device__ static double load(const W* w, uint64_t e) { return (double)__ldg(w + e); }
+};
+template <>
+struct WeightIO<void> {
+    __device__ static double load(const void*, uint64_t) { return 1.0; }
+};
+template <class W>
+constexpr int weight_bytes() { return sizeof(W); }
+template <>
+constexpr int weight_bytes<void>() { return 0; }
+
+}  // namespace ggb

@@ -1,0 +1,115 @@
+// exchange.cu — NCCL transport for the partitioned engine (see exchange.cuh).
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include "exchange.cuh"
+#include "kernels.cuh"
+
+namespace ggb {
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string load_error;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            load_error = dlerror() ? dlerror() : "dlopen libnccl.so.2 failed";
+            return;
+        }
+#define GGB_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+        GGB_SYM(GetUniqueId, "ncclGetUniqueId");
+        GGB_SYM(CommInitRank, "ncclCommInitRank");
+        GGB_SYM(CommDestroy, "ncclCommDestroy");
+        GGB_SYM(Broadcast, "ncclBroadcast");
+        GGB_SYM(AllReduce, "ncclAllReduce");
+        GGB_SYM(GroupStart, "ncclGroupStart");
+        GGB_SYM(GroupEnd, "ncclGroupEnd");
+        GGB_SYM(GetErrorString, "ncclGetErrorString");
+#undef GGB_SYM
+    });
+    if (!api.GetUniqueId || !api.CommInitRank || !api.Broadcast || !api.AllReduce)
+        throw Error(GG_NCCL, "NCCL unavailable: " + load_error);
+    return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+        throw Error(GG_NCCL, std::string(what) + ": " + s);
+    }
+}
+
+void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size) {
+    if (g.nranks <= 1) return;
+    if (!g.exchange || !g.exchange->comm) throw Error(GG_NCCL, "multi-rank graph without exchange");
+    const NcclApi& api = nccl();
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int r = 0; r < g.nranks; ++r) {
+        const uint64_t b = g.bounds[r], e = g.bounds[r + 1];
+        if (e == b) continue;
+        char* p = static_cast<char*>(global_buf) + b * elem_size;
+        nccl_check(api.Broadcast(p, p, (e - b) * elem_size, ncclChar, r, g.exchange->comm, g.stream),
+                   "ncclBroadcast");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+}
+
+void exchange_counters(DevGraph& g, void* ctr_v) {
+    if (g.nranks <= 1) return;
+    const NcclApi& api = nccl();
+    IterCounters* ctr = static_cast<IterCounters*>(ctr_v);
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    nccl_check(api.AllReduce(&ctr->gathered, &ctr->gathered, 2, ncclUint64, ncclSum,
+                             g.exchange->comm, g.stream), "allreduce(edges)");
+    nccl_check(api.AllReduce(&ctr->changed, &ctr->changed, 2, ncclUint32, ncclSum,
+                             g.exchange->comm, g.stream), "allreduce(changed)");
+    nccl_check(api.AllReduce(&ctr->bad_min, &ctr->bad_min, 1, ncclUint32, ncclMin,
+                             g.exchange->comm, g.stream), "allreduce(bad)");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+}
+
+}  // namespace ggb
+
+extern "C" {
+
+gg_status gg_nccl_unique_id(uint8_t out[128]) {
+    return ggb::guarded(nullptr, [&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        ggb::nccl_check(ggb::nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, &id, 128);
+    });
+}
+
+gg_status gg_exchange_nccl_create(const uint8_t unique_id[128], int rank, int nranks,
+                                  gg_exchange** out, gg_error* err) {
+    return ggb::guarded(err, [&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks)
+            throw ggb::Error(GG_INVALID_ARGUMENT, "rank/nranks out of range");
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, 128);
+        auto* x = new gg_exchange;
+        x->rank = rank;
+        x->nranks = nranks;
+        ncclResult_t r = ggb::nccl().CommInitRank(&x->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            delete x;
+            ggb::nccl_check(r, "ncclCommInitRank");
+        }
+        *out = x;
+    });
+}
+
+gg_status gg_exchange_destroy(gg_exchange* x) {
+    return ggb::guarded(nullptr, [&] {
+        if (!x) return;
+        if (x->comm) ggb::nccl().CommDestroy(x->comm);
+        delete x;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,40 @@
+// exchange.cuh — the per-iteration exchange of the 1-D destination
+// partition: every rank owns a 32-aligned, edge-balanced
+// destination range and a full replica of the message (property) vector.
+// After each iteration the owned slices of msg_next are all-gathered
+// (grouped ncclBroadcast per root = AllGatherV over NVLink/NVSwitch) and the
+// iteration counters are all-reduced, so every rank takes the same early-exit
+// and EngineError decisions (engine.hpp:226-240).
+#pragma once
+
+#include <nccl.h>
+
+#include "graph.cuh"
+
+struct gg_exchange {
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+};
+
+namespace ggb {
+
+// libnccl.so.2 is dlopen'ed on first multi-GPU use (the single-GPU path has
+// no NCCL dependency and never clashes with the NCCL torch already loaded).
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl();
+
+void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size);
+void exchange_counters(DevGraph& g, void* ctr);
+
+}  // namespace ggb

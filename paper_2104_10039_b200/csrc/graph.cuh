@@ -1,0 +1,120 @@
+// graph.cuh — HBM-resident pull CSC (gg::Graph, graph.hpp:29-49) and the
+// per-graph device workspace.
+//
+// HBM layout per rank (local = owned destination range [v_begin, v_end)):
+//   off      u64[nloc+1]   local in-edge offsets (rebased to 0)
+//   src      u32[e_loc]    in-edge sources, GLOBAL vertex ids
+//   w        W[e_loc]      none | u32 | f32 | f64
+//   outdeg   u32[n]        out-degree of every (global) vertex
+//   tasks    uint4[]       {window, chunk, nchunks, slot} work list of the full CSC
+//   mtasks   uint4[]       the chunks of multi-chunk windows
+// Run workspace (allocated once, reused across runs):
+//   bitmap   u32[e_loc/32+1] active-edge flags (EdgeFlags, graph.hpp:54-72,
+//                            one BIT per edge instead of one byte)
+//   wprefix  u64[words+1]    exclusive popcount prefix of the bitmap
+//   s_off/s_src/s_w          sparsified CSC (only flagged edges, same order)
+//   s_tasks/s_mtasks         its work lists
+//   msg[2], prop, status[2], partials, tickets, counters
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct gg_exchange;
+
+namespace ggb {
+
+struct DevBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+// Simple grow-only named workspace: runs reuse device memory, so no
+// cudaMalloc happens inside a timed run after the first one.
+struct Workspace {
+    std::map<std::string, DevBuffer> bufs;
+    void* get(const std::string& name, size_t bytes) {
+        DevBuffer& b = bufs[name];
+        if (b.bytes < bytes || !b.ptr) {
+            if (b.ptr) GGB_CUDA(cudaFree(b.ptr));
+            b.ptr = nullptr;
+            b.bytes = 0;
+            GGB_CUDA(cudaMalloc(&b.ptr, bytes ? bytes : 16));
+            b.bytes = bytes ? bytes : 16;
+        }
+        return b.ptr;
+    }
+    template <class T>
+    T* get(const std::string& name, size_t count) {
+        return static_cast<T*>(get(name, count * sizeof(T)));
+    }
+    void release() {
+        for (auto& kv : bufs)
+            if (kv.second.ptr) cudaFree(kv.second.ptr);
+        bufs.clear();
+    }
+};
+
+// Work list: uint4 {window, chunk, nchunks, partial slot of chunk 0 (or ~0)}.
+struct TaskList {
+    uint4* tasks = nullptr;      // all tasks
+    uint32_t ntasks = 0;
+    uint4* mtasks = nullptr;     // tasks of windows with > 1 chunk (slot order)
+    uint32_t nmtasks = 0;
+};
+
+struct DevGraph {
+    int device = 0;
+    int rank = 0, nranks = 1;
+    gg_exchange* exchange = nullptr;
+    uint64_t n = 0, e_global = 0;
+    uint64_t v_begin = 0, v_end = 0, nloc = 0;
+    uint64_t e_base = 0, e_loc = 0;        // global id of first local edge, local count
+    std::vector<uint64_t> bounds;          // vertex bounds of every rank (nranks+1)
+    std::vector<uint64_t> ebounds;         // edge bounds of every rank
+    uint64_t* off = nullptr;
+    uint32_t* src = nullptr;
+    void* w = nullptr;
+    gg_weight_kind wkind = GG_W_NONE;
+    uint32_t* outdeg = nullptr;
+    TaskList full;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    Workspace ws;
+    ~DevGraph();
+};
+
+size_t weight_size(gg_weight_kind k);
+
+// A full CSC generated on device (rmat.cu).
+struct RmatCsc {
+    uint64_t n = 0, e = 0;
+    uint64_t* off = nullptr;
+    uint32_t* src = nullptr;
+    void* w = nullptr;
+    uint32_t* outdeg = nullptr;
+};
+RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st);
+void bp_priors_device(uint64_t n, uint64_t seed, float* out, cudaStream_t st);
+
+// Build {window, chunk} work lists for a list with local offsets `off`.
+void build_tasks(DevGraph& g, const uint64_t* off, const std::string& tag, TaskList& out);
+// flags -> sparsified CSC (s_off/s_src/s_w) + its task list. Returns kept edges.
+uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
+                        void* s_w, TaskList& out, const std::string& tag,
+                        cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
+// engine.cpp:63-75 sparsify into a bitmap over local edges (global ids hashed).
+void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones);
+// Deferred superstep bad-vertex scan.
+void launch_superstep_invalid(DevGraph& g, const uint8_t* st_cur, const uint8_t* st_next,
+                              const uint64_t* s_off, void* ctr);
+int occupancy_grid(const void* kernel, int block, size_t smem, int num_sms);
+
+}  // namespace ggb
+
+struct gg_dev_graph {
+    ggb::DevGraph g;
+};

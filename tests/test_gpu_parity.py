@@ -1,0 +1,288 @@
+"""Device engine vs CPU oracle on seeded inputs (the parity tests proper).
+
+Mirrors the reference's own tests (test_engine.cpp, test_algorithms.cpp,
+acceptance_main.cpp) through the C ABI, plus R-MAT cases at the BASELINE
+configs' shapes (reduced scale where the oracle must finish in seconds)."""
+import numpy as np
+import pytest
+
+from oracle.oracle import BP, BP_EDGE, GG, PR, SSSP, WCC, Oracle
+from tests.parity import compare, to_graph
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["accurate", "sp", "sms", "gg"]
+
+
+# --------------------------------------------------------------------------
+# known answers (test_algorithms.cpp / test_engine.cpp restated)
+# --------------------------------------------------------------------------
+def test_pagerank_four_cycle_fixed_point(ggb):  # test_algorithms.cpp:76-83, test_engine.cpp:184-194
+    g = Oracle.build_graph(4, [0, 1, 2, 3], [1, 2, 3, 0])
+    rep = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(), ggb.EngineConfig(max_iterations=50))
+    assert rep.iterations_run == 1
+    np.testing.assert_allclose(rep.final_properties, 0.25, rtol=1e-12)
+
+
+def test_pagerank_star_hub(ggb):  # test_algorithms.cpp:85-97
+    g = Oracle.build_graph(4, [0, 1, 2], [3, 3, 3])
+    rep = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(0.85, 1e-16),
+                  ggb.EngineConfig(max_iterations=300))
+    assert rep.final_properties[3] == pytest.approx(0.0375 + 0.85 * 3 * 0.0375)
+
+
+def test_sp_sigma_zero_leak(ggb):  # test_engine.cpp:122-131
+    g = Oracle.dumbbell(2)
+    rep = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(),
+                  ggb.EngineConfig("sp", sigma=0.0, max_iterations=50))
+    np.testing.assert_allclose(rep.final_properties, 0.15 / 4, rtol=1e-12)
+    assert rep.iterations_run == 2
+
+
+def test_three_cycle_gathers_every_edge(ggb):  # test_engine.cpp:226-237
+    g = Oracle.build_graph(3, [0, 1, 2], [1, 2, 0])
+    rep = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(0.85, 1e-15),
+                  ggb.EngineConfig(max_iterations=5))
+    assert all(r.processed_edges == 3 and r.active_vertices == 3 for r in rep.per_iteration)
+
+
+def test_unreachable_theta_deactivates_every_edge(ggb):  # test_engine.cpp:239-256
+    g = Oracle.dumbbell(3)
+    rep = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(),
+                  ggb.EngineConfig("gg", sigma=1.0, theta=2.0, alpha=5, max_iterations=10))
+    assert rep.per_iteration[5].mode == ggb.IterationMode.superstep
+    for r in rep.per_iteration[6:]:
+        assert r.mode == ggb.IterationMode.approximate and r.processed_edges == 0
+    np.testing.assert_allclose(rep.final_properties, 0.15 / 6, rtol=1e-12)
+
+
+def test_sssp_known_answers(ggb):  # test_algorithms.cpp:140-152
+    g = Oracle.build_graph(3, [0, 1], [1, 2])
+    rep = ggb.run(to_graph(ggb, g), ggb.sssp_spec(0), ggb.EngineConfig(max_iterations=10))
+    assert list(rep.final_properties) == [0.0, 1.0, 2.0]
+    g = Oracle.build_graph(3, [0], [1])
+    rep = ggb.run(to_graph(ggb, g), ggb.sssp_spec(0), ggb.EngineConfig(max_iterations=10))
+    assert np.isinf(rep.final_properties[2])
+
+
+def test_sssp_source_out_of_range(ggb):  # test_algorithms.cpp:173-177
+    with pytest.raises(ValueError, match="sssp source vertex out of range"):
+        ggb.run(to_graph(ggb, Oracle.dumbbell(2)), ggb.sssp_spec(99), ggb.EngineConfig(max_iterations=5))
+
+
+def test_wcc_known_answers(ggb):  # test_algorithms.cpp:189-201
+    g = Oracle.build_graph(3, [0, 1, 2], [1, 2, 0])
+    assert list(ggb.run(to_graph(ggb, g), ggb.wcc_spec(),
+                        ggb.EngineConfig(max_iterations=10)).final_properties) == [0, 0, 0]
+    g = Oracle.build_graph(4, [0, 1, 2, 3], [1, 0, 3, 2])
+    assert list(ggb.run(to_graph(ggb, g), ggb.wcc_spec(),
+                        ggb.EngineConfig(max_iterations=10)).final_properties) == [0, 0, 2, 2]
+
+
+def test_bp_isolated_and_uninformative(ggb, oracle):  # test_algorithms.cpp:232-255
+    g = Oracle.build_graph(3, [0], [1])
+    rep = ggb.run(to_graph(ggb, g), ggb.bp_spec(), ggb.EngineConfig(max_iterations=20))
+    ref = Oracle.run(g, BP, max_iterations=20)
+    np.testing.assert_allclose(rep.final_properties[2], ref.props[2], rtol=1e-14)
+    g = Oracle.build_graph(2, [0, 1], [1, 0])
+    rep = ggb.run(to_graph(ggb, g), ggb.bp_spec(2, 0.5, 1e-9), ggb.EngineConfig(max_iterations=30))
+    prior = Oracle.run(Oracle.build_graph(2, [], []), BP, max_iterations=1, coupling=0.5).props
+    np.testing.assert_allclose(rep.final_properties, prior, rtol=1e-12)
+
+
+def test_bp_beliefs_normalised(ggb):  # test_algorithms.cpp:273-284
+    g = Oracle.power_law(200, 5.0, 2.2, 8)
+    for budget in (1, 2, 5, 10):
+        rep = ggb.run(to_graph(ggb, g), ggb.bp_spec(3, 0.7, 1e-9),
+                      ggb.EngineConfig(max_iterations=budget))
+        assert np.all(np.abs(rep.final_properties.sum(axis=1) - 1.0) <= 1e-12)
+
+
+def test_empty_graph(ggb):  # test_engine.cpp:304-309
+    g = ggb.Graph(0, np.zeros(1, np.uint64), np.zeros(0, np.uint32))
+    rep = ggb.run(g, ggb.pagerank_spec(), ggb.EngineConfig())
+    assert rep.iterations_run == 0 and rep.final_properties.size == 0
+
+
+def test_invalid_config_names_field(ggb):  # test_engine.cpp:105-120
+    g = to_graph(ggb, Oracle.dumbbell(2))
+    with pytest.raises(ValueError, match="sigma"):
+        ggb.run(g, ggb.pagerank_spec(), ggb.EngineConfig(sigma=1.5))
+    with pytest.raises(ValueError, match="alpha"):
+        ggb.run(g, ggb.pagerank_spec(), ggb.EngineConfig(sigma=0.5, alpha=0))
+
+
+def test_invalid_property_abort(ggb):
+    # engine.hpp:226-233: a negative weight drives SSSP distances below 0
+    # (SsspProgram::valid, algorithms.hpp:82) -> EngineError(t, smallest v).
+    g = Oracle.random_graph(60, 400, 3, True)
+    w = g.w.copy()
+    w[::37] = -5.0
+    g.w = w
+    compare(ggb, g, SSSP, max_iterations=50)
+    compare(ggb, g, SSSP, scheme="gg", sigma=0.6, theta=0.1, alpha=2, max_iterations=50, seed=4)
+
+
+# --------------------------------------------------------------------------
+# exactness gate and random-graph parity (acceptance 1, 2, 10)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_exactness_gate(ggb, seed):  # acceptance_main.cpp:80-113
+    g = Oracle.power_law(1000, 8.0, 2.1, seed)
+    u = Oracle.symmetrized(g)
+    for prog, graph in ((PR, g), (SSSP, g), (WCC, u), (BP, g)):
+        base = compare(ggb, graph, prog, max_iterations=20)[0].final_properties
+        for scheme in ("gg", "sp"):
+            rep = compare(ggb, graph, prog, scheme=scheme, sigma=1.0, alpha=20, max_iterations=20,
+                          seed=seed)[0]
+            assert np.array_equal(rep.final_properties, base)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_random_graphs_all_programs(ggb, scheme, seed):
+    g = Oracle.power_law(500, 8.0, 2.1, seed)
+    gw = Oracle.random_graph(300, 3000, seed, True)
+    u = Oracle.symmetrized(g)
+    kw = dict(scheme=scheme, sigma=0.5, theta=0.1, alpha=3, max_iterations=30, seed=seed)
+    total = 0
+    total += compare(ggb, g, PR, **kw)[2]
+    total += compare(ggb, gw, SSSP, **kw)[2]
+    total += compare(ggb, gw, SSSP, graded=True, **kw)[2]
+    total += compare(ggb, u, WCC, **kw)[2]
+    total += compare(ggb, g, BP, **kw)[2]
+    total += compare(ggb, g, BP, states=3, coupling=0.7, **kw)[2]
+    assert total == 0
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_edge_bp_fp32(ggb, seed):
+    g = Oracle.power_law(600, 8.0, 2.1, seed)
+    c = Oracle.bp_couplings(g.e, seed)
+    gw = Oracle.build_graph(g.n, g.src, np.repeat(np.arange(g.n), np.diff(g.off.astype(np.int64))),
+                            c.astype(np.float64))
+    pri = Oracle.bp_priors(g.n, seed)
+    for scheme in SCHEMES:
+        _, _, mism = compare(ggb, gw, BP_EDGE, scheme=scheme, sigma=0.5, theta=0.01, alpha=4,
+                             max_iterations=30, seed=seed, prior_table=pri, device_weights=c)
+        assert mism == 0
+
+
+def test_sssp_u32_weights_exact(ggb):
+    g = Oracle.rmat(12, 16, 2)
+    w = Oracle.rmat_weights_u32(g.e, 2)
+    gw = Oracle.build_graph(g.n, g.src, np.repeat(np.arange(g.n), np.diff(g.off.astype(np.int64))),
+                            w.astype(np.float64))
+    src = int(np.argmax(gw.outdeg))
+    for scheme in SCHEMES:
+        compare(ggb, gw, SSSP, scheme=scheme, sigma=0.5, theta=0.05, alpha=4, seed=2,
+                max_iterations=g.n + 1, source=src, graded=True, device_weights=w)
+
+
+def test_hub_windows_multi_chunk(ggb):
+    # in-degree 5000 hub + 3000 hub: windows split into several chunks, and
+    # the superstep hub pass evaluates their influences with chunk carries.
+    rng = np.random.default_rng(5)
+    n = 6000
+    src = np.concatenate([rng.integers(0, n, 5000), rng.integers(0, n, 3000),
+                          rng.integers(0, n, 20000)]).astype(np.uint32)
+    dst = np.concatenate([np.full(5000, 3), np.full(3000, 40),
+                          rng.integers(0, n, 20000)]).astype(np.uint32)
+    g = Oracle.build_graph(n, src, dst)
+    u = Oracle.symmetrized(g)
+    for scheme in SCHEMES:
+        kw = dict(scheme=scheme, sigma=0.5, theta=0.001, alpha=2, max_iterations=25, seed=7)
+        assert compare(ggb, g, PR, **kw)[2] == 0
+        assert compare(ggb, u, WCC, **kw)[2] == 0
+        assert compare(ggb, g, BP, **kw)[2] == 0
+
+
+def test_dumbbell_recovery(ggb):  # test_engine.cpp:258-286, acceptance 3
+    k = 8
+    g = Oracle.dumbbell(k)
+    exact = compare(ggb, g, WCC, max_iterations=64)[0].final_properties
+    # the reference's find_bridge_dropping_seed (test_support.hpp:198-228)
+    bridge = [e for v in range(g.n) for e in range(int(g.off[v]), int(g.off[v + 1]))
+              if (g.src[e], v) in ((k - 1, k), (k, k - 1))]
+    seed = None
+    for s in range(512):
+        f = Oracle.sparsify(g.e, 0.5, s)
+        if any(f[e] for e in bridge):
+            continue
+        if all(f[int(g.off[v]):int(g.off[v + 1])].any() for v in range(g.n)):
+            seed = s
+            break
+    assert seed is not None
+    sp = compare(ggb, g, WCC, scheme="sp", sigma=0.5, max_iterations=64, seed=seed)[0]
+    assert not np.array_equal(sp.final_properties, exact)
+    gg = compare(ggb, g, WCC, scheme="gg", sigma=0.5, theta=0.5, alpha=2, max_iterations=64,
+                 seed=seed)[0]
+    assert np.array_equal(gg.final_properties, exact)
+    assert gg.per_iteration[2].mode == ggb.IterationMode.superstep
+
+
+def test_thread_and_launch_invariance(ggb):  # test_engine.cpp:161-182 analogue
+    g = Oracle.power_law(2000, 8.0, 2.1, 3)
+    cfg = ggb.EngineConfig("gg", 0.4, 0.2, 3, 30, 5)
+    a = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(), cfg)
+    cfg8 = ggb.EngineConfig("gg", 0.4, 0.2, 3, 30, 5, threads=8)
+    b = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(), cfg8)
+    assert np.array_equal(a.final_properties, b.final_properties)
+    assert [r.processed_edges for r in a.per_iteration] == [r.processed_edges for r in b.per_iteration]
+
+
+# --------------------------------------------------------------------------
+# R-MAT inputs (BASELINE configs at oracle-sized scales)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("scale,ef,seed,sym,wk", [(10, 16, 1, False, None), (12, 16, 2, False, "u32"),
+                                                 (11, 16, 3, True, None), (12, 8, 4, False, "coupling")])
+def test_device_rmat_equals_oracle(ggb, scale, ef, seed, sym, wk):
+    dg = ggb.DeviceGraph.rmat(scale, ef, seed, symmetrize=sym, weights=wk)
+    h = dg.to_host()
+    g = Oracle.rmat(scale, ef, seed)
+    if sym:
+        g = Oracle.symmetrized(g)
+    assert np.array_equal(h.in_offsets, g.off) and np.array_equal(h.in_sources, g.src)
+    assert np.array_equal(h.out_degree, g.outdeg)
+    if wk == "u32":
+        assert np.array_equal(h.weights, Oracle.rmat_weights_u32(g.e, seed))
+    if wk == "coupling":
+        assert np.array_equal(h.weights, Oracle.bp_couplings(g.e, seed))
+
+
+def test_c1_pagerank_rmat_s16(ggb):
+    """BASELINE configs[0]: PR gg on R-MAT s16 EF16 seed 1, d=0.85, eps=1e-7,
+    theta=0.01 (sigma 0.5, alpha 4; budget = accurate iterations_run)."""
+    g = Oracle.rmat(16, 16, 1)
+    assert g.e == 955529
+    acc = compare(ggb, g, PR, max_iterations=50)[0]
+    _, ref, mism = compare(ggb, g, PR, scheme="gg", sigma=0.5, theta=0.01, alpha=4,
+                           max_iterations=acc.iterations_run, seed=1)
+    assert mism == 0
+
+
+def test_rmat_sssp_wcc_bp_small(ggb):
+    g = Oracle.rmat(13, 16, 2)
+    w = Oracle.rmat_weights_u32(g.e, 2)
+    gw = Oracle.build_graph(g.n, g.src, np.repeat(np.arange(g.n), np.diff(g.off.astype(np.int64))),
+                            w.astype(np.float64))
+    compare(ggb, gw, SSSP, scheme="gg", sigma=0.5, theta=0.05, alpha=4, seed=2,
+            max_iterations=g.n + 1, source=0, graded=True, device_weights=w)
+    u = Oracle.symmetrized(Oracle.rmat(13, 16, 3))
+    compare(ggb, u, WCC, scheme="gg", sigma=0.5, theta=0.0, alpha=4, seed=3, max_iterations=u.n + 1)
+    g4 = Oracle.rmat(12, 16, 4)
+    c = Oracle.bp_couplings(g4.e, 4)
+    g4w = Oracle.build_graph(g4.n, g4.src, np.repeat(np.arange(g4.n), np.diff(g4.off.astype(np.int64))),
+                             c.astype(np.float64))
+    compare(ggb, g4w, BP_EDGE, scheme="gg", sigma=0.5, theta=0.01, alpha=4, seed=4,
+            max_iterations=30, prior_table=Oracle.bp_priors(g4.n, 4), device_weights=c)
+
+
+def test_device_sparsify_matches_reference_hash(ggb):  # engine.cpp:63-75, test_engine.cpp:54-80
+    e = 100000
+    a = ggb.sparsify(e, 0.5, 3)
+    assert np.array_equal(a, Oracle.sparsify(e, 0.5, 3))
+    assert 49000 <= int(a.sum()) <= 51000
+    assert int(ggb.sparsify(e, 1.0, 9).sum()) == e and int(ggb.sparsify(e, 0.0, 9).sum()) == 0
+    lo, hi = ggb.sparsify(2000, 0.3, 5), ggb.sparsify(2000, 0.7, 5)
+    assert np.all(hi[lo == 1] == 1)
