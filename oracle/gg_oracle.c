@@ -215,71 +215,99 @@ static inline void rmat_edge(uint64_t key, uint64_t i, uint32_t scale, double t1
     *ps = s; *pd = d;
 }
 
-static int cmp_u32(const void* a, const void* b) {
-    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
     return x < y ? -1 : x > y;
 }
 
+/* Two-level bucketing, contention free: per-thread counts by the top
+ * `bbits` destination bits, a regenerate-and-scatter pass of (dst,src) keys,
+ * then each bucket sorted and de-duplicated independently. */
 og_graph* og_rmat(uint32_t scale, uint32_t edge_factor, uint64_t seed,
                   double a, double b, double c, int threads) {
     if (scale < 1 || scale > 31) return NULL;
 #ifdef _OPENMP
     if (threads > 0) omp_set_num_threads(threads);
+    const int T = omp_get_max_threads();
 #else
     (void)threads;
+    const int T = 1;
 #endif
     const uint64_t n = 1ull << scale;
     const uint64_t m = (uint64_t)edge_factor << scale;
     const double t1 = a, t2 = a + b, t3 = a + b + c;
     const uint64_t key = og_mix64(seed);
-    uint64_t* cnt = (uint64_t*)xcalloc(n + 1, 8);
-    /* pass 1: count per dst (self-loops dropped) */
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < (int64_t)m; ++i) {
-        uint32_t s, d;
-        rmat_edge(key, (uint64_t)i, scale, t1, t2, t3, &s, &d);
-        if (s == d) continue;
-#pragma omp atomic
-        cnt[d + 1]++;
+    const uint32_t bbits = scale < 16 ? scale : 16;
+    const uint32_t bshift = scale - bbits;
+    const uint64_t B = 1ull << bbits;
+    uint64_t* cnt = (uint64_t*)xcalloc((size_t)T * B + 1, 8); /* [bucket][thread] */
+#pragma omp parallel num_threads(T)
+    {
+#ifdef _OPENMP
+        const int t = omp_get_thread_num();
+#else
+        const int t = 0;
+#endif
+        const uint64_t lo = m * (uint64_t)t / (uint64_t)T, hi = m * (uint64_t)(t + 1) / (uint64_t)T;
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint32_t s, d;
+            rmat_edge(key, i, scale, t1, t2, t3, &s, &d);
+            if (s == d) continue;
+            cnt[(uint64_t)(d >> bshift) * T + t]++;
+        }
     }
-    for (uint64_t v = 0; v < n; ++v) cnt[v + 1] += cnt[v];
-    const uint64_t mm = cnt[n];
-    uint32_t* bucket = (uint32_t*)xmalloc(mm * 4 + 4);
-    uint64_t* cur = (uint64_t*)xmalloc(n * 8);
-    memcpy(cur, cnt, n * 8);
-    /* pass 2: regenerate (counter-based) and scatter sources into dst buckets */
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < (int64_t)m; ++i) {
-        uint32_t s, d;
-        rmat_edge(key, (uint64_t)i, scale, t1, t2, t3, &s, &d);
-        if (s == d) continue;
-        uint64_t p;
-#pragma omp atomic capture
-        p = cur[d]++;
-        bucket[p] = s;
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < (uint64_t)T * B; ++i) { uint64_t x = cnt[i]; cnt[i] = total; total += x; }
+    cnt[(uint64_t)T * B] = total;
+    uint64_t* keys = (uint64_t*)xmalloc(total * 8 + 8);
+#pragma omp parallel num_threads(T)
+    {
+#ifdef _OPENMP
+        const int t = omp_get_thread_num();
+#else
+        const int t = 0;
+#endif
+        const uint64_t lo = m * (uint64_t)t / (uint64_t)T, hi = m * (uint64_t)(t + 1) / (uint64_t)T;
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint32_t s, d;
+            rmat_edge(key, i, scale, t1, t2, t3, &s, &d);
+            if (s == d) continue;
+            keys[cnt[(uint64_t)(d >> bshift) * T + t]++] = ((uint64_t)d << 32) | s;
+        }
     }
-    free(cur);
-    /* per bucket: sort by src, drop duplicates */
-    uint64_t* ucnt = (uint64_t*)xcalloc(n + 1, 8);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t v = 0; v < (int64_t)n; ++v) {
-        uint32_t* p = bucket + cnt[v];
-        uint64_t len = cnt[v + 1] - cnt[v];
-        if (len > 1) qsort(p, len, 4, cmp_u32);
+    /* after pass 2, cnt[b*T + t] is the end of (b, t); bucket b = [start, end) */
+    uint64_t* bstart = (uint64_t*)xmalloc((B + 1) * 8);
+    uint64_t* ucnt = (uint64_t*)xcalloc(B + 1, 8);
+    bstart[0] = 0;
+    for (uint64_t bk = 0; bk < B; ++bk) bstart[bk + 1] = cnt[bk * T + (T - 1)];
+    free(cnt);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(T)
+    for (int64_t bk = 0; bk < (int64_t)B; ++bk) {
+        uint64_t* p = keys + bstart[bk];
+        const uint64_t len = bstart[bk + 1] - bstart[bk];
+        if (len > 1) qsort(p, len, 8, cmp_u64);
         uint64_t k = 0;
         for (uint64_t j = 0; j < len; ++j)
             if (j == 0 || p[j] != p[j - 1]) p[k++] = p[j];
-        ucnt[v + 1] = k;
+        ucnt[bk + 1] = k;
     }
-    for (uint64_t v = 0; v < n; ++v) ucnt[v + 1] += ucnt[v];
+    for (uint64_t bk = 0; bk < B; ++bk) ucnt[bk + 1] += ucnt[bk];
     og_graph* g = (og_graph*)xcalloc(1, sizeof(og_graph));
-    g->n = n; g->e = ucnt[n];
-    g->off = ucnt;
+    g->n = n; g->e = ucnt[B];
+    g->off = (uint64_t*)xcalloc(n + 1, 8);
     g->src = (uint32_t*)xmalloc(g->e * 4 + 4);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t v = 0; v < (int64_t)n; ++v)
-        memcpy(g->src + ucnt[v], bucket + cnt[v], (ucnt[v + 1] - ucnt[v]) * 4);
-    free(bucket); free(cnt);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(T)
+    for (int64_t bk = 0; bk < (int64_t)B; ++bk) {
+        const uint64_t* p = keys + bstart[bk];
+        const uint64_t len = ucnt[bk + 1] - ucnt[bk];
+        uint64_t o = ucnt[bk];
+        for (uint64_t j = 0; j < len; ++j) {
+            g->src[o + j] = (uint32_t)p[j];
+            g->off[(p[j] >> 32) + 1]++; /* dst owned by this bucket only */
+        }
+    }
+    for (uint64_t v = 0; v < n; ++v) g->off[v + 1] += g->off[v];
+    free(keys); free(bstart); free(ucnt);
     g->w = NULL;
     g->outdeg = (uint32_t*)xcalloc(n, 4);
     for (uint64_t e = 0; e < g->e; ++e) g->outdeg[g->src[e]]++;

@@ -238,7 +238,8 @@ gg_status gg_dev_graph_export(const gg_dev_graph* h, uint64_t* offsets, uint32_t
     return guarded(nullptr, [&] {
         if (!h) throw Error(GG_INVALID_ARGUMENT, "null graph");
         const DevGraph& g = h->g;
-        if (g.nranks != 1) throw Error(GG_INVALID_ARGUMENT, "export needs a single-rank graph");
+        if (g.nranks != 1 && (offsets || sources || weights))  // out_degree is replicated
+            throw Error(GG_INVALID_ARGUMENT, "CSC export needs a single-rank graph");
         GGB_CUDA(cudaSetDevice(g.device));
         if (offsets) GGB_CUDA(cudaMemcpy(offsets, g.off, (g.nloc + 1) * 8, cudaMemcpyDeviceToHost));
         if (sources && g.e_loc)

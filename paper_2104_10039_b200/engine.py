@@ -153,17 +153,25 @@ class DeviceGraph:
         L.lib().gg_dev_graph_info(self._h, *[C.byref(v) for v in vals])
         return dict(zip(("n", "e", "v_begin", "v_end", "e_local"), (v.value for v in vals)))
 
-    def to_host(self) -> Graph:
+    def to_host(self, alloc=None) -> Graph:
+        """Copy the CSC back to host arrays made by alloc(count, dtype)
+        (default np.empty; pass a pinned allocator for fast re-uploads)."""
+        alloc = alloc or (lambda count, dt: np.empty(count, dt))
         n, e = self.n, self.e
-        off = np.zeros(n + 1, np.uint64)
-        src = np.zeros(max(e, 1), np.uint32)
-        od = np.zeros(max(n, 1), np.uint32)
+        off = alloc(n + 1, np.uint64)
+        src = alloc(max(e, 1), np.uint32)
+        od = alloc(max(n, 1), np.uint32)
         wd = getattr(self, "weight_dtype", None)
-        w = np.zeros(max(e, 1), wd) if wd is not None else None
+        w = alloc(max(e, 1), wd) if wd is not None else None
         _raise(L.lib().gg_dev_graph_export(self._h, off.ctypes.data, src.ctypes.data,
                                            w.ctypes.data if w is not None else None,
                                            od.ctypes.data), None)
         return Graph(n, off, src[:e], None if w is None else w[:e], od[:n])
+
+    def out_degree(self) -> np.ndarray:
+        od = np.zeros(max(self.n, 1), np.uint32)
+        _raise(L.lib().gg_dev_graph_export(self._h, None, None, None, od.ctypes.data), None)
+        return od[:self.n]
 
     def close(self):
         if self._h:
@@ -317,9 +325,12 @@ def unpack_bitmap(words: np.ndarray, e: int) -> np.ndarray:
 
 
 def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: bool = False,
-        rec_cap: int | None = None) -> RunReport:
+        rec_cap: int | None = None, device_output: bool = False) -> RunReport:
     """gg::run (engine.hpp:141-249) on the device. `graph` is a Graph
-    (uploaded for the call) or a DeviceGraph (already resident)."""
+    (uploaded for the call) or a DeviceGraph (already resident).
+    timing: CUDA-event time of every kernel into the records.
+    device_output: leave the final properties in HBM (no D2H copy;
+    final_properties is then None)."""
     ccfg = cfg.c()
     owned = None
     if isinstance(graph, Graph):
@@ -333,7 +344,8 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         recs = (L.IterRecordC * max(cap, 1))()
         summ = L.RunSummaryC()
         flags = np.zeros(max((e + 31) // 32, 1), np.uint32) if want_flags else None
-        opts = L.RunOptsC(flags.ctypes.data if flags is not None else None, int(timing), 0)
+        opts = L.RunOptsC(flags.ctypes.data if flags is not None else None, int(timing),
+                          int(device_output))
         err = L.ErrorC()
         lib = L.lib()
         if isinstance(program, PageRankProgram):
@@ -373,7 +385,8 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
                                float(recs[i].kernel_ms), float(recs[i].rebuild_ms),
                                float(recs[i].exchange_ms), int(recs[i].algo_bytes))
                for i in range(k)]
-        return RunReport(props if n else props[:0], int(summ.iterations_run), per,
+        out_props = None if device_output else (props if n else props[:0])
+        return RunReport(out_props, int(summ.iterations_run), per,
                          float(summ.total_wall_seconds), int(summ.total_processed_edges),
                          int(summ.kept_edges), int(summ.kernel_launches),
                          unpack_bitmap(flags, e) if flags is not None else None)
@@ -423,6 +436,39 @@ def stretch_error(approx, exact) -> ErrorReport:
         raise RuntimeError("stretch_error: approximate distance below exact (engine bug)")
     _raise(rc, None)
     return ErrorReport("stretch", out.value, (1.0 - out.value) * 100.0)
+
+
+class Exchange:
+    """NCCL transport of the 1-D destination partition (one process per GPU).
+    Rank 0 makes the id (Exchange.unique_id()); the caller broadcasts it
+    (e.g. torch.distributed.broadcast_object_list) and every rank builds
+    Exchange(rank, nranks, uid) before creating its DeviceGraph."""
+
+    def __init__(self, rank: int, nranks: int, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        err = L.ErrorC()
+        _raise(L.lib().gg_exchange_nccl_create(buf, rank, nranks, C.byref(h), C.byref(err)), err)
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _raise(L.lib().gg_nccl_unique_id(buf), None)
+        return bytes(buf)
+
+    def close(self):
+        if self.handle:
+            L.lib().gg_exchange_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+def bp_priors(n: int, seed: int) -> np.ndarray:
+    """BASELINE C4 priors generated on the device: float32[n, 2]."""
+    out = np.zeros(2 * max(n, 1), np.float32)
+    _raise(L.lib().gg_bp_priors(n, seed, out.ctypes.data), None)
+    return out[:2 * n].reshape(n, 2)
 
 
 def partition_plan(g: Graph, nranks: int) -> np.ndarray:
