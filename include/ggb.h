@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GGB_ABI_VERSION 1
+#define GGB_ABI_VERSION 2
 
 typedef enum gg_status {
     GG_OK = 0,
@@ -87,10 +87,14 @@ typedef struct gg_iter_record {
     uint64_t processed_edges;
     uint64_t active_vertices;
     double wall_seconds;        /* host wall time of the iteration */
-    double kernel_ms;           /* CUDA-event time of the gather kernel(s) */
+    double kernel_ms;           /* CUDA-event time of the gather step (edge + vertex kernels) */
     double rebuild_ms;          /* CUDA-event time of the sparse rebuild (supersteps) */
     double exchange_ms;         /* multi-GPU exchange time (0 for 1 GPU) */
-    uint64_t algo_bytes;        /* algorithmic HBM bytes of the gather kernel(s) */
+    uint64_t algo_bytes;        /* algorithmic HBM bytes of the gather step */
+    double edge_ms;             /* edge kernel (+ superstep pass 2) */
+    double vertex_ms;           /* vertex epilogue kernel */
+    uint64_t edge_bytes;        /* algorithmic bytes of the edge kernel: E_p * b_e */
+    uint64_t vertex_bytes;      /* algorithmic bytes of the vertex kernel: N * b_v */
 } gg_iter_record;
 
 typedef struct gg_run_summary {

@@ -43,7 +43,9 @@ class IterRecordC(C.Structure):
     _fields_ = [("mode", C.c_int32), ("processed_edges", C.c_uint64),
                 ("active_vertices", C.c_uint64), ("wall_seconds", C.c_double),
                 ("kernel_ms", C.c_double), ("rebuild_ms", C.c_double),
-                ("exchange_ms", C.c_double), ("algo_bytes", C.c_uint64)]
+                ("exchange_ms", C.c_double), ("algo_bytes", C.c_uint64),
+                ("edge_ms", C.c_double), ("vertex_ms", C.c_double),
+                ("edge_bytes", C.c_uint64), ("vertex_bytes", C.c_uint64)]
 
 
 class RunSummaryC(C.Structure):

@@ -1,5 +1,6 @@
-// build.cu — flag set maintenance: sparsify, bitmap -> sparsified CSC
-// compaction, work-list construction, deferred superstep validity scan.
+// build.cu — flag-set maintenance and list layout: sparsify, bitmap ->
+// sparsified CSC compaction, the run -> vertex map of a list, and the
+// deferred superstep validity scan.
 //
 // The reference keeps one flag BYTE per edge and re-tests it inside every
 // approximate iteration (engine.hpp:203). Here the flags are a bitmap that
@@ -9,6 +10,7 @@
 // unchanged and no flag is read on the hot path.
 #include <cub/cub.cuh>
 
+#include "exchange.cuh"
 #include "graph.cuh"
 #include "kernels.cuh"
 
@@ -73,62 +75,74 @@ void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed,
 }
 
 // --------------------------------------------------------------------------
-// work lists
+// List layout: the non-empty vertices (nz_vid / nz_start) and the run map
+// run_i[r] = max{i : nz_start[i] + pad <= first valid position of run r}
+// (= the non-empty vertex containing it): every non-empty vertex marks the
+// first run whose first valid position is >= its start, then a max-scan.
 // --------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t window_chunks(uint64_t edges) {
-    const uint64_t nrows = (edges + 31) >> 5;
-    return nrows > (uint64_t)kRowsPerChunk
-               ? (uint32_t)((nrows + kRowsPerChunk - 1) / kRowsPerChunk) : 1u;
+__global__ void nonempty_flag_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
+                                     uint32_t* __restrict__ flag) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= nloc;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        flag[v] = v < nloc && off[v + 1] > off[v] ? 1u : 0u;
 }
 
-__global__ void task_count_kernel(const uint64_t* __restrict__ off, uint64_t nloc, uint64_t nwin,
-                                  uint64_t* __restrict__ cnt) {
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w <= nwin;
-         w += (uint64_t)gridDim.x * blockDim.x) {
-        if (w == nwin) { cnt[w] = 0; continue; }
-        const uint64_t v0 = w * kWindow;
-        const uint64_t v1 = v0 + kWindow < nloc ? v0 + kWindow : nloc;
-        const uint32_t nch = window_chunks(off[v1] - off[v0]);
-        cnt[w] = (uint64_t)nch | (nch > 1 ? (uint64_t)nch << 32 : 0ull);
-    }
-}
-
-__global__ void task_fill_kernel(const uint64_t* __restrict__ pref, uint64_t nwin,
-                                 uint4* __restrict__ tasks, uint4* __restrict__ mtasks) {
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwin;
-         w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p0 = pref[w], p1 = pref[w + 1];
-        const uint32_t first = (uint32_t)p0, nch = (uint32_t)p1 - first;
-        const uint32_t mfirst = (uint32_t)(p0 >> 32);
-        for (uint32_t c = 0; c < nch; ++c) {
-            const uint4 t = make_uint4((uint32_t)w, c, nch, nch > 1 ? mfirst : 0xffffffffu);
-            tasks[first + c] = t;
-            if (nch > 1) mtasks[mfirst + c] = t;
+__global__ void nonempty_fill_kernel(const uint64_t* __restrict__ off, uint64_t nloc, uint64_t pad,
+                                     const uint32_t* __restrict__ idx, uint64_t nruns,
+                                     uint32_t* __restrict__ nz_vid, uint64_t* __restrict__ nz_start,
+                                     uint32_t* __restrict__ marks) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= nloc;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        if (v == nloc) {
+            nz_start[idx[nloc]] = off[nloc];  // sentinel: end of the last vertex
+            continue;
         }
+        if (off[v + 1] <= off[v]) continue;
+        const uint32_t i = idx[v];
+        nz_vid[i] = (uint32_t)v;
+        nz_start[i] = off[v];
+        const uint64_t s = off[v] + pad;
+        const uint64_t r = s <= pad ? 0 : (s + kRun - 1) / kRun;
+        if (r < nruns) atomicMax(marks + r, i);
     }
 }
 
-void build_tasks(DevGraph& g, const uint64_t* off, const std::string& tag, TaskList& out) {
-    const uint64_t nwin = (g.nloc + kWindow - 1) / kWindow;
-    uint64_t* cnt = g.ws.get<uint64_t>(tag + ".cnt", nwin + 1);
-    uint64_t* pref = g.ws.get<uint64_t>(tag + ".pref", nwin + 1);
-    task_count_kernel<<<grid_for(nwin + 1, 256), 256, 0, g.stream>>>(off, g.nloc, nwin, cnt);
+struct MaxU32 {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e, const std::string& tag,
+                ListMeta& meta) {
+    meta.pad = pad;
+    meta.e = e;
+    meta.ntasks = (pad + e + kChunkEdges - 1) / kChunkEdges;
+    if (e == 0) meta.ntasks = 0;
+    meta.nruns = meta.ntasks * kWarp;
+    uint32_t* flag = g.ws.get<uint32_t>(tag + ".nzflag", g.nloc + 1);
+    uint32_t* idx = g.ws.get<uint32_t>(tag + ".nzidx", g.nloc + 1);
+    uint32_t* marks = g.ws.get<uint32_t>(tag + ".runmark", meta.nruns + 1);
+    meta.run_i = g.ws.get<uint32_t>(tag + ".run_i", meta.nruns + 1);
+    nonempty_flag_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(off, g.nloc, flag);
     GGB_CUDA(cudaGetLastError());
-    size_t tmp = 0;
-    GGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, pref, nwin + 1, g.stream));
-    void* tmpp = g.ws.get("cub.tmp." + tag, tmp);
-    GGB_CUDA(cub::DeviceScan::ExclusiveSum(tmpp, tmp, cnt, pref, nwin + 1, g.stream));
-    uint64_t total = 0;
-    GGB_CUDA(cudaMemcpyAsync(&total, pref + nwin, 8, cudaMemcpyDeviceToHost, g.stream));
+    size_t tmp = 0, tmp2 = 0;
+    GGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag, idx, g.nloc + 1, g.stream));
+    GGB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp2, marks, meta.run_i, MaxU32{},
+                                            meta.nruns ? meta.nruns : 1, g.stream));
+    void* tmpp = g.ws.get("cub.tmp." + tag, std::max(tmp, tmp2));
+    GGB_CUDA(cub::DeviceScan::ExclusiveSum(tmpp, tmp, flag, idx, g.nloc + 1, g.stream));
+    uint32_t nz = 0;
+    GGB_CUDA(cudaMemcpyAsync(&nz, idx + g.nloc, 4, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
-    out.ntasks = (uint32_t)total;
-    out.nmtasks = (uint32_t)(total >> 32);
-    out.tasks = g.ws.get<uint4>(tag + ".tasks", out.ntasks + 1);
-    out.mtasks = g.ws.get<uint4>(tag + ".mtasks", out.nmtasks + 1);
-    if (nwin)
-        task_fill_kernel<<<grid_for(nwin, 256), 256, 0, g.stream>>>(pref, nwin, out.tasks,
-                                                                    out.mtasks);
+    meta.nz = nz;
+    meta.nz_vid = g.ws.get<uint32_t>(tag + ".nz_vid", (uint64_t)nz + 1);
+    meta.nz_start = g.ws.get<uint64_t>(tag + ".nz_start", (uint64_t)nz + 1);
+    if (meta.nruns) GGB_CUDA(cudaMemsetAsync(marks, 0, meta.nruns * 4, g.stream));
+    nonempty_fill_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(
+        off, g.nloc, pad, idx, meta.nruns, meta.nz_vid, meta.nz_start, marks);
     GGB_CUDA(cudaGetLastError());
+    if (!meta.nruns) return;
+    GGB_CUDA(cub::DeviceScan::InclusiveScan(tmpp, tmp2, marks, meta.run_i, MaxU32{}, meta.nruns,
+                                            g.stream));
 }
 
 // --------------------------------------------------------------------------
@@ -158,29 +172,36 @@ __global__ void soff_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
 
 template <int WB>
 __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w,
-                               uint64_t e_loc, const uint32_t* __restrict__ bitmap,
+                               uint64_t e_loc, uint64_t in_pad, const uint32_t* __restrict__ bitmap,
                                const uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
-                               void* __restrict__ s_w) {
+                               void* __restrict__ s_w, uint64_t out_pad) {
     // warp-aligned: lane == e & 31, so the word and its prefix are shared
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < e_loc;
          e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t word = __ldg(bitmap + (e >> 5));
         const uint32_t b = (uint32_t)(e & 31);
         if ((word >> b) & 1u) {
-            const uint64_t pos = __ldg(wpref + (e >> 5)) + (uint64_t)__popc(word & ((1u << b) - 1u));
-            s_src[pos] = __ldg(src + e);
+            const uint64_t pos = out_pad + __ldg(wpref + (e >> 5)) +
+                                 (uint64_t)__popc(word & ((1u << b) - 1u));
+            s_src[pos] = __ldg(src + in_pad + e);
             if constexpr (WB == 4)
-                static_cast<uint32_t*>(s_w)[pos] = __ldg(static_cast<const uint32_t*>(w) + e);
+                static_cast<uint32_t*>(s_w)[pos] =
+                    __ldg(static_cast<const uint32_t*>(w) + in_pad + e);
             if constexpr (WB == 8)
                 static_cast<unsigned long long*>(s_w)[pos] =
-                    __ldg(static_cast<const unsigned long long*>(w) + e);
+                    __ldg(static_cast<const unsigned long long*>(w) + in_pad + e);
         }
     }
 }
 
+uint64_t sparse_pad(DevGraph& g, uint64_t kept_local) {
+    if (g.nranks <= 1) return 0;
+    return exchange_exclusive_base(g, kept_local) % kChunkEdges;
+}
+
 uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
-                        void* s_w, TaskList& out, const std::string& tag, cudaEvent_t ev0,
-                        cudaEvent_t ev1, int* launches) {
+                        void* s_w, ListMeta& meta, cudaEvent_t ev0, cudaEvent_t ev1,
+                        int* launches) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
     uint64_t* cnt = g.ws.get<uint64_t>("rb.cnt", nwords + 1);
     uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
@@ -194,23 +215,27 @@ uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, ui
     soff_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref,
                                                                   s_off);
     GGB_CUDA(cudaGetLastError());
+    uint64_t kept = 0;
+    GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    const uint64_t pad = sparse_pad(g, kept);
     const size_t wb = weight_size(g.wkind);
     const unsigned gr = grid_for(g.e_loc, 256, 148ull * 16 * 8);
     if (g.e_loc) {
         if (wb == 0)
-            compact_kernel<0><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, bitmap, wpref, s_src, s_w);
+            compact_kernel<0><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
+                                                        wpref, s_src, s_w, pad);
         else if (wb == 4)
-            compact_kernel<4><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, bitmap, wpref, s_src, s_w);
+            compact_kernel<4><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
+                                                        wpref, s_src, s_w, pad);
         else
-            compact_kernel<8><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, bitmap, wpref, s_src, s_w);
+            compact_kernel<8><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
+                                                        wpref, s_src, s_w, pad);
         GGB_CUDA(cudaGetLastError());
     }
-    build_tasks(g, s_off, tag, out);
+    build_runs(g, s_off, pad, kept, "sp", meta);
     if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-    if (launches) *launches += 6;
-    uint64_t kept = 0;
-    GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
-    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    if (launches) *launches += 7;
     return kept;
 }
 
@@ -235,6 +260,9 @@ void launch_superstep_invalid(DevGraph& g, const uint8_t* st_cur, const uint8_t*
 
 DevGraph::~DevGraph() {
     ws.release();
+    if (h_ctr) cudaFreeHost(h_ctr);
+    for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
     if (off) cudaFree(off);
     if (src) cudaFree(src);
     if (w) cudaFree(w);

@@ -119,23 +119,26 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                                       csc->offsets ? csc->offsets + csc->n + 1 : nullptr);
             if (off.empty()) off.assign(1, 0);
             finish_graph(g, off);
+            const uint64_t pad = g.e_base % kChunkEdges;  // padded = global position mod 512
             GGB_CUDA(cudaMalloc(&g.off, (g.nloc + 1) * 8));
-            GGB_CUDA(cudaMalloc(&g.src, (g.e_loc + 1) * 4));
+            GGB_CUDA(cudaMalloc(&g.src, (pad + g.e_loc + kRun) * 4));
             GGB_CUDA(cudaMalloc(&g.outdeg, (g.n + 1) * 4));
             std::vector<uint64_t> loc(g.nloc + 1);
             for (uint64_t i = 0; i <= g.nloc; ++i) loc[i] = off[g.v_begin + i] - g.e_base;
             GGB_CUDA(cudaMemcpyAsync(g.off, loc.data(), (g.nloc + 1) * 8, cudaMemcpyHostToDevice,
                                      g.stream));
             if (g.e_loc)
-                GGB_CUDA(cudaMemcpyAsync(g.src, csc->sources + g.e_base, g.e_loc * 4,
+                GGB_CUDA(cudaMemcpyAsync(g.src + pad, csc->sources + g.e_base, g.e_loc * 4,
                                          cudaMemcpyHostToDevice, g.stream));
             const size_t wb = weight_size(g.wkind);
             if (wb) {
-                GGB_CUDA(cudaMalloc(&g.w, (g.e_loc + 1) * wb));
+                GGB_CUDA(cudaMalloc(&g.w, (pad + g.e_loc + kRun) * wb));
                 if (g.e_loc)
-                    GGB_CUDA(cudaMemcpyAsync(g.w, static_cast<const char*>(csc->weights) + g.e_base * wb,
+                    GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
+                                             static_cast<const char*>(csc->weights) + g.e_base * wb,
                                              g.e_loc * wb, cudaMemcpyHostToDevice, g.stream));
             }
+            g.full.pad = pad;
             if (csc->out_degree) {
                 if (g.n)
                     GGB_CUDA(cudaMemcpyAsync(g.outdeg, csc->out_degree, g.n * 4,
@@ -152,7 +155,7 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                                              g.stream));
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
             }
-            build_tasks(g, g.off, "full", g.full);
+            build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
             delete h;
@@ -187,21 +190,24 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
                 rebase_kernel<<<256, 256, 0, g.stream>>>(r.off + g.v_begin, g.nloc + 1, g.e_base,
                                                           g.off);
                 GGB_CUDA(cudaGetLastError());
-                GGB_CUDA(cudaMalloc(&g.src, (g.e_loc + 1) * 4));
-                GGB_CUDA(cudaMemcpyAsync(g.src, r.src + g.e_base, g.e_loc * 4,
+                const uint64_t pad = g.e_base % kChunkEdges;
+                GGB_CUDA(cudaMalloc(&g.src, (pad + g.e_loc + kRun) * 4));
+                GGB_CUDA(cudaMemcpyAsync(g.src + pad, r.src + g.e_base, g.e_loc * 4,
                                          cudaMemcpyDeviceToDevice, g.stream));
                 const size_t wb = weight_size(g.wkind);
                 if (wb) {
-                    GGB_CUDA(cudaMalloc(&g.w, (g.e_loc + 1) * wb));
-                    GGB_CUDA(cudaMemcpyAsync(g.w, static_cast<char*>(r.w) + g.e_base * wb,
+                    GGB_CUDA(cudaMalloc(&g.w, (pad + g.e_loc + kRun) * wb));
+                    GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
+                                             static_cast<char*>(r.w) + g.e_base * wb,
                                              g.e_loc * wb, cudaMemcpyDeviceToDevice, g.stream));
                 }
+                g.full.pad = pad;
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
                 cudaFree(r.off);
                 cudaFree(r.src);
                 if (r.w) cudaFree(r.w);
             }
-            build_tasks(g, g.off, "full", g.full);
+            build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
             delete h;
@@ -243,10 +249,11 @@ gg_status gg_dev_graph_export(const gg_dev_graph* h, uint64_t* offsets, uint32_t
         GGB_CUDA(cudaSetDevice(g.device));
         if (offsets) GGB_CUDA(cudaMemcpy(offsets, g.off, (g.nloc + 1) * 8, cudaMemcpyDeviceToHost));
         if (sources && g.e_loc)
-            GGB_CUDA(cudaMemcpy(sources, g.src, g.e_loc * 4, cudaMemcpyDeviceToHost));
+            GGB_CUDA(cudaMemcpy(sources, g.src + g.full.pad, g.e_loc * 4, cudaMemcpyDeviceToHost));
         const size_t wb = weight_size(g.wkind);
         if (weights && wb && g.e_loc)
-            GGB_CUDA(cudaMemcpy(weights, g.w, g.e_loc * wb, cudaMemcpyDeviceToHost));
+            GGB_CUDA(cudaMemcpy(weights, static_cast<const char*>(g.w) + g.full.pad * wb,
+                                g.e_loc * wb, cudaMemcpyDeviceToHost));
         if (out_degree && g.n)
             GGB_CUDA(cudaMemcpy(out_degree, g.outdeg, g.n * 4, cudaMemcpyDeviceToHost));
     });

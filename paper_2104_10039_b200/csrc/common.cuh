@@ -19,9 +19,10 @@ namespace ggb {
 
 constexpr int kWarp = 32;
 constexpr int kWindow = 32;              // vertices per window (one per lane)
-constexpr int kRowsPerChunk = 32;        // rows of 32 edges per warp task
-constexpr int kChunkEdges = kWarp * kRowsPerChunk;
-constexpr int kBlockThreads = 256;
+constexpr int kRun = 16;                 // consecutive in-edges folded by one lane
+constexpr int kChunkEdges = kWarp * kRun;  // in-edges per warp task (512)
+constexpr int kRowsPerChunk = kChunkEdges / 32;
+constexpr int kBlockThreads = 128;
 constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 
 // splitmix64 finalizer: engine.cpp:9-14 (bit-identical on host and device).
@@ -166,6 +167,47 @@ __device__ __forceinline__ M ld_msg(const M* p, uint64_t pol) {
         out = *p;
     }
     return out;
+}
+
+// ---- cp.async (LDGSTS): global -> shared without registers, so one warp can
+// keep hundreds of independent gathers in flight.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, uint64_t pol) {
+    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                     :: "r"(smem_u32(smem)), "l"(gmem), "l"(pol) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;"
+                     :: "r"(smem_u32(smem)), "l"(gmem), "n"(BYTES), "l"(pol) : "memory");
+}
+// Copy one trivially copyable element of any 4-byte-granular size.
+template <class T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem, uint64_t pol) {
+    static_assert(sizeof(T) % 4 == 0, "4-byte granular");
+    char* d = reinterpret_cast<char*>(smem);
+    const char* s = reinterpret_cast<const char*>(gmem);
+    if constexpr (sizeof(T) % 16 == 0) {
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(T) / 16); ++i) cp_async<16>(d + 16 * i, s + 16 * i, pol);
+    } else if constexpr (sizeof(T) % 8 == 0) {
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(T) / 8); ++i) cp_async<8>(d + 8 * i, s + 8 * i, pol);
+    } else {
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(T) / 4); ++i) cp_async<4>(d + 4 * i, s + 4 * i, pol);
+    }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 // L2-coherent load of data written by other CTAs in the same kernel

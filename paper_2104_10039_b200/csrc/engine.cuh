@@ -44,7 +44,7 @@ struct RunIO {
     uint64_t rec_cap = 0;
     gg_run_summary* sum = nullptr;
     const gg_run_opts* opts = nullptr;
-    void* out_props = nullptr;   // host: double[n*S] or uint32[n] (kRawOut)
+    void* out_props = nullptr;   // host: double[n*S] or uint32[n] (kRawOutput)
     int out_states = 1;
 };
 
@@ -80,53 +80,49 @@ inline unsigned grid1d(uint64_t n, int block = 256) {
     return (unsigned)(g ? g : 1);
 }
 
-struct EventPair {
-    cudaEvent_t a = nullptr, b = nullptr;
-    void make() {
-        if (!a) {
-            GGB_CUDA(cudaEventCreate(&a));
-            GGB_CUDA(cudaEventCreate(&b));
-        }
-    }
-    ~EventPair() {
-        if (a) cudaEventDestroy(a);
-        if (b) cudaEventDestroy(b);
-    }
-    double ms() const {
-        float f = 0.f;
-        GGB_CUDA(cudaEventElapsedTime(&f, a, b));
-        return (double)f;
-    }
-};
+inline double event_ms(cudaEvent_t a, cudaEvent_t b) {
+    float f = 0.f;
+    GGB_CUDA(cudaEventElapsedTime(&f, a, b));
+    return (double)f;
+}
 
 template <class P, class W>
 struct Engine {
     using Prop = typename P::Property;
     using Msg = typename P::Message;
     using Acc = typename P::Accum;
-    static constexpr int U = sizeof(Msg) <= 8 ? 4 : 2;
 
-    static int grid_main(DevGraph& g, bool super) {
-        static int cached[2] = {0, 0};
-        int& c = cached[super ? 1 : 0];
-        if (!c) {
-            const void* k = super ? (const void*)iteration_kernel<P, W, true, U>
-                                  : (const void*)iteration_kernel<P, W, false, U>;
-            c = occupancy_grid(k, kBlockThreads, 0, g.num_sms);
-        }
-        return c;
+    template <int MODE>
+    static int grid_edge(DevGraph& g) {
+        static int cached = 0;
+        if (!cached) cached = occupancy_grid((const void*)edge_kernel<P, W, MODE>, kBlockThreads, 0,
+                                             g.num_sms);
+        return cached;
+    }
+    static int grid_pass2(DevGraph& g) {
+        static int cached = 0;
+        if (!cached) cached = occupancy_grid((const void*)edge_pass2_kernel<P, W>, kBlockThreads, 0,
+                                             g.num_sms);
+        return cached;
     }
 
-    // Algorithmic HBM bytes of one gather launch (SURVEY §8(d) byte formula:
-    // E_p * b_e + N * b_v, superstep adds the bitmap write E_p / 8).
-    static uint64_t algo_bytes(uint64_t edges, uint64_t nloc, bool super) {
+    // Algorithmic HBM bytes (SURVEY §8(d) byte formula B = E_p*b_e + N*b_v;
+    // a superstep adds the bitmap write E_p/8).
+    static uint64_t edge_bytes(uint64_t edges, bool super) {
         const uint64_t be = 4 + sizeof(Msg) + (uint64_t)weight_bytes<W>();
+        return edges * be + (super ? edges / 8 : 0);
+    }
+    static uint64_t vertex_bytes(uint64_t nloc) {
         uint64_t bv = 8 + 2 + 2 * sizeof(Prop) + (P::kMsgIsProp ? 0 : sizeof(Msg)) +
                       (P::kNeedsDegree ? 4 : 0);
         if constexpr (requires { P::kReadsPrior; }) bv += 8;
-        uint64_t b = edges * be + nloc * bv;
-        if (super) b += edges / 8;
-        return b;
+        return nloc * bv;
+    }
+
+    template <int MODE>
+    static void launch_edge(DevGraph& g, const EdgeArgs<P, W>& ea) {
+        edge_kernel<P, W, MODE><<<grid_edge<MODE>(g), kBlockThreads, 0, g.stream>>>(ea);
+        GGB_CUDA(cudaGetLastError());
     }
 
     static void run(DevGraph& g, const P& prog, RunIO& io) {
@@ -142,32 +138,23 @@ struct Engine {
         Prop* prop = P::kMsgIsProp ? nullptr : ws.get<Prop>("prop", nloc);
         uint8_t* st[2] = {ws.get<uint8_t>("st0", nloc + 1), ws.get<uint8_t>("st1", nloc + 1)};
         IterCounters* ctr = ws.get<IterCounters>("ctr", 1);
+        IterCounters* h_ctr = static_cast<IterCounters*>(g.host_counters(sizeof(IterCounters)));
+        Acc* acc_out = ws.get<Acc>("acc_out", nloc + 1);
+        const uint64_t ntask_cap = g.full.ntasks + 2;
+        Acc* hv = ws.get<Acc>("hv", ntask_cap);
+        Acc* tv = ws.get<Acc>("tv", ntask_cap);
+        Acc* carry = ws.get<Acc>("carry", ntask_cap);
         const uint64_t nwords = (g.e_loc + 31) / 32;
         const size_t wsz = (size_t)weight_bytes<W>();
         uint32_t* bitmap = nullptr;
         uint64_t* s_off = nullptr;
         uint32_t* s_src = nullptr;
         void* s_w = nullptr;
-        TaskList sp;
-        const uint64_t nwin = (nloc + kWindow - 1) / kWindow;
-        // partial slots: the full list has the most multi-chunk tasks
-        Acc* partials = ws.get<Acc>("partials", ((uint64_t)g.full.nmtasks + 1) * kWindow);
-        uint32_t* tickets;
-        {
-            const bool fresh = ws.bufs.find("tickets") == ws.bufs.end() ||
-                               ws.bufs["tickets"].bytes < (nwin + 1) * 4;
-            tickets = ws.get<uint32_t>("tickets", nwin + 1);
-            if (fresh) GGB_CUDA(cudaMemsetAsync(tickets, 0, (nwin + 1) * 4, g.stream));
-        }
-        IterCounters* h_ctr = nullptr;
-        GGB_CUDA(cudaHostAlloc(&h_ctr, sizeof(IterCounters), cudaHostAllocDefault));
-        struct HostFree {
-            IterCounters* p;
-            ~HostFree() { cudaFreeHost(p); }
-        } hf{h_ctr};
-
-        EventPair ev_k, ev_rb, ev_x;
-        if (timing) { ev_k.make(); ev_rb.make(); ev_x.make(); }
+        ListMeta sp;
+        cudaEvent_t e0 = timing ? g.event(0) : nullptr, e1 = timing ? g.event(1) : nullptr;
+        cudaEvent_t e2 = timing ? g.event(2) : nullptr, e3 = timing ? g.event(3) : nullptr;
+        cudaEvent_t e4 = timing ? g.event(4) : nullptr, e5 = timing ? g.event(5) : nullptr;
+        cudaEvent_t e6 = timing ? g.event(6) : nullptr, e7 = timing ? g.event(7) : nullptr;
 
         init_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, n, (uint32_t)g.v_begin,
                                                          (uint32_t)nloc, g.outdeg, msg[0], prop,
@@ -178,27 +165,14 @@ struct Engine {
         if (sparse) {  // engine.hpp:151-161
             bitmap = ws.get<uint32_t>("bitmap", nwords + 1);
             s_off = ws.get<uint64_t>("s_off", nloc + 1);
-            s_src = ws.get<uint32_t>("s_src", g.e_loc + 1);
-            s_w = wsz ? ws.get("s_w", (g.e_loc + 1) * wsz) : nullptr;
+            s_src = ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
+            s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
             sparsify_bitmap(g, bitmap, cfg.sigma, cfg.seed, false);
             ++launches;
-            kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, "sp", nullptr, nullptr, &launches);
+            kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches);
         }
         const uint64_t* a_off = sparse ? s_off : g.off;
-
-        IterArgs<P, W> a{};
-        a.prog = prog;
-        a.n = n;
-        a.v_begin = (uint32_t)g.v_begin;
-        a.nloc = (uint32_t)nloc;
-        a.a_off = a_off;
-        a.prop = prop;
-        a.outdeg = g.outdeg;
-        a.bitmap = bitmap;
-        a.theta = cfg.theta;
-        a.partials = partials;
-        a.win_ticket = tickets;
-        a.ctr = ctr;
+        const uint32_t hot_limit = (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg));
 
         int cur = 0;
         uint64_t iterations_run = 0, total_edges = 0;
@@ -208,53 +182,91 @@ struct Engine {
             const int mode = mode_for(cfg.scheme, t, cfg.alpha);
             const bool approx = mode == GG_MODE_APPROXIMATE;
             const bool super = mode == GG_MODE_SUPERSTEP;
-            if (approx) {
-                a.g_off = s_off; a.g_src = s_src; a.g_w = static_cast<const W*>(s_w);
-                a.tasks = sp.tasks; a.ntasks = sp.ntasks;
-            } else {
-                a.g_off = g.off; a.g_src = g.src; a.g_w = static_cast<const W*>(g.w);
-                a.tasks = g.full.tasks; a.ntasks = g.full.ntasks;
-            }
-            a.msg_cur = msg[cur]; a.msg_next = msg[cur ^ 1];
-            a.st_cur = st[cur]; a.st_next = st[cur ^ 1];
+            const ListMeta& L = approx ? sp : g.full;
+            EdgeArgs<P, W> ea{};
+            ea.prog = prog;
+            ea.src = approx ? s_src : g.src;
+            ea.w = static_cast<const W*>(approx ? s_w : g.w);
+            ea.run_i = L.run_i;
+            ea.nz_vid = L.nz_vid;
+            ea.nz_start = L.nz_start;
+            ea.pad = L.pad;
+            ea.e_end = L.e_end();
+            ea.ntasks = L.ntasks;
+            ea.nruns = L.nruns;
+            ea.nz = L.nz;
+            ea.a_off = a_off;
+            ea.st_cur = st[cur];
+            ea.msg_cur = msg[cur];
+            ea.hot_limit = hot_limit;
+            ea.acc_out = acc_out;
+            ea.hv = hv;
+            ea.tv = tv;
+            ea.carry = carry;
+            ea.bitmap = bitmap;
+            ea.theta = cfg.theta;
+            VertexArgs<P, W> va{};
+            va.prog = prog;
+            va.n = n;
+            va.v_begin = (uint32_t)g.v_begin;
+            va.nloc = (uint32_t)nloc;
+            va.off = approx ? s_off : g.off;
+            va.pad = L.pad;
+            va.a_off = a_off;
+            va.st_cur = st[cur];
+            va.st_next = st[cur ^ 1];
+            va.prop = prop;
+            va.msg_cur = msg[cur];
+            va.msg_next = msg[cur ^ 1];
+            va.outdeg = g.outdeg;
+            va.acc_out = acc_out;
+            va.hv = hv;
+            va.tv = tv;
+            va.carry = carry;
+            va.ctr = ctr;
+
             GGB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
             GGB_CUDA(cudaMemsetAsync(&ctr->bad_min, 0xff, 4, g.stream));
-            if (timing) GGB_CUDA(cudaEventRecord(ev_k.a, g.stream));
-            if (super) {
-                iteration_kernel<P, W, true, U><<<grid_main(g, true), kBlockThreads, 0, g.stream>>>(a);
-                GGB_CUDA(cudaGetLastError());
+            if (timing) GGB_CUDA(cudaEventRecord(e0, g.stream));
+            if (L.ntasks) {
+                // every edge of the sparsified list (and of the full list under
+                // the accurate scheme) belongs to a processed vertex
+                const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
+                if (super) launch_edge<kEdgeSuper>(g, ea);
+                else if (all_proc) launch_edge<kEdgePlain>(g, ea);
+                else launch_edge<kEdgeCheck>(g, ea);
                 ++launches;
-                if (g.full.nmtasks) {
-                    superstep_hub_kernel<P, W, U><<<grid_main(g, true), kBlockThreads, 0, g.stream>>>(
-                        a, g.full.mtasks, g.full.nmtasks);
-                    GGB_CUDA(cudaGetLastError());
-                    ++launches;
-                }
-            } else {
-                iteration_kernel<P, W, false, U><<<grid_main(g, false), kBlockThreads, 0, g.stream>>>(a);
+            }
+            if (timing) GGB_CUDA(cudaEventRecord(e1, g.stream));
+            if (super) vertex_kernel<P, W, true><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            else vertex_kernel<P, W, false><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            GGB_CUDA(cudaGetLastError());
+            ++launches;
+            if (timing) GGB_CUDA(cudaEventRecord(e2, g.stream));
+            if (super && L.ntasks) {  // flags of vertices whose fold began in an earlier task
+                edge_pass2_kernel<P, W><<<grid_pass2(g), kBlockThreads, 0, g.stream>>>(ea);
                 GGB_CUDA(cudaGetLastError());
                 ++launches;
             }
-            if (timing) GGB_CUDA(cudaEventRecord(ev_k.b, g.stream));
+            if (timing) GGB_CUDA(cudaEventRecord(e3, g.stream));
             double rb_ms = 0.0;
             if (super) {  // new flag set -> new sparsified CSC (engine.hpp:207-214)
-                kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, "sp",
-                                      timing ? ev_rb.a : nullptr, timing ? ev_rb.b : nullptr,
-                                      &launches);
-                if (timing) rb_ms = ev_rb.ms();
+                kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, timing ? e4 : nullptr,
+                                      timing ? e5 : nullptr, &launches);
                 GGB_CUDA(cudaMemcpyAsync(h_ctr, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
                                          g.stream));
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
+                if (timing) rb_ms = event_ms(e4, e5);
                 if (h_ctr->any_invalid) {
                     launch_superstep_invalid(g, st[cur], st[cur ^ 1], s_off, ctr);
                     ++launches;
                 }
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
-                if (timing) GGB_CUDA(cudaEventRecord(ev_x.a, g.stream));
+                if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
                 exchange_slices(g, msg[cur ^ 1], sizeof(Msg));
                 exchange_counters(g, ctr);
-                if (timing) GGB_CUDA(cudaEventRecord(ev_x.b, g.stream));
+                if (timing) GGB_CUDA(cudaEventRecord(e7, g.stream));
             }
             GGB_CUDA(cudaMemcpyAsync(h_ctr, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
                                      g.stream));
@@ -280,10 +292,16 @@ struct Engine {
                 r.processed_edges = h_ctr->gathered;
                 r.active_vertices = h_ctr->processed;
                 r.wall_seconds = wall;
-                r.kernel_ms = timing ? ev_k.ms() : 0.0;
+                r.edge_ms = timing ? event_ms(e0, e1) + event_ms(e2, e3) : 0.0;
+                r.vertex_ms = timing ? event_ms(e1, e2) : 0.0;
+                r.kernel_ms = r.edge_ms + r.vertex_ms;
                 r.rebuild_ms = rb_ms;
-                r.exchange_ms = (timing && g.nranks > 1) ? ev_x.ms() : 0.0;
-                r.algo_bytes = algo_bytes(h_ctr->gathered, g.n, super);
+                r.exchange_ms = (timing && g.nranks > 1) ? event_ms(e6, e7) : 0.0;
+                // per-rank algorithmic bytes of this rank's launches
+                const uint64_t local_edges = approx ? kept : g.e_loc;
+                r.edge_bytes = edge_bytes(local_edges, super);
+                r.vertex_bytes = vertex_bytes(nloc);
+                r.algo_bytes = r.edge_bytes + r.vertex_bytes;
             }
             iterations_run = t;
             total_edges += h_ctr->gathered;
@@ -293,19 +311,15 @@ struct Engine {
         }
 
         // final properties (engine.hpp:243)
-        const Prop* final_local;
         Prop* final_all;
         if constexpr (P::kMsgIsProp) {
             final_all = msg[cur];  // exchanged every iteration: full on every rank
-            final_local = final_all + g.v_begin;
         } else {
             final_all = ws.get<Prop>("final", n);
             GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
                                      cudaMemcpyDeviceToDevice, g.stream));
             if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
-            final_local = prop;
         }
-        (void)final_local;
         if (io.out_props && !(io.opts && io.opts->device_output)) {
             if constexpr (requires { P::kRawOutput; }) {  // WCC: uint32 labels as-is
                 GGB_CUDA(cudaMemcpyAsync(io.out_props, final_all, n * 4, cudaMemcpyDeviceToHost,

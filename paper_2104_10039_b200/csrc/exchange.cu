@@ -58,6 +58,24 @@ void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size) {
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }
 
+uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
+    if (g.nranks <= 1) return 0;
+    const NcclApi& api = nccl();
+    uint64_t* d = g.ws.get<uint64_t>("xbase", (uint64_t)g.nranks + 1);
+    GGB_CUDA(cudaMemcpyAsync(d + g.rank, &local, 8, cudaMemcpyHostToDevice, g.stream));
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int r = 0; r < g.nranks; ++r)
+        nccl_check(api.Broadcast(d + r, d + r, 1, ncclUint64, r, g.exchange->comm, g.stream),
+                   "ncclBroadcast(kept)");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    std::vector<uint64_t> h(g.nranks);
+    GGB_CUDA(cudaMemcpyAsync(h.data(), d, 8 * g.nranks, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    uint64_t base = 0;
+    for (int r = 0; r < g.rank; ++r) base += h[r];
+    return base;
+}
+
 void exchange_counters(DevGraph& g, void* ctr_v) {
     if (g.nranks <= 1) return;
     const NcclApi& api = nccl();

@@ -36,5 +36,7 @@ const NcclApi& nccl();
 
 void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size);
 void exchange_counters(DevGraph& g, void* ctr);
+// sum of `local` over ranks below this one (allgather of one u64 per rank)
+uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local);
 
 }  // namespace ggb

@@ -58,12 +58,22 @@ struct Workspace {
     }
 };
 
-// Work list: uint4 {window, chunk, nchunks, partial slot of chunk 0 (or ~0)}.
-struct TaskList {
-    uint4* tasks = nullptr;      // all tasks
-    uint32_t ntasks = 0;
-    uint4* mtasks = nullptr;     // tasks of windows with > 1 chunk (slot order)
-    uint32_t nmtasks = 0;
+// Edge-centric layout of one list (full or sparsified CSC): padded
+// positions P = pad + local edge index, runs of 16 and tasks of 512 padded
+// positions, run_v[r] = local vertex containing the first valid position of
+// run r (see kernels.cuh).
+// The edge kernel walks only the list's NON-EMPTY vertices (nz_vid / nz_start,
+// a doubly-compressed view), so long stretches of empty vertices cost nothing.
+struct ListMeta {
+    uint64_t pad = 0;      // padded position of local edge 0 (global position mod 512)
+    uint64_t e = 0;        // local edges
+    uint64_t nruns = 0;    // ntasks * 32 (every run index of a task is addressable)
+    uint64_t ntasks = 0;
+    uint64_t nz = 0;       // non-empty vertices
+    uint32_t* run_i = nullptr;     // [nruns] index into nz_* of the vertex at the run's first position
+    uint32_t* nz_vid = nullptr;    // [nz] local vertex id
+    uint64_t* nz_start = nullptr;  // [nz+1] local edge offset (nz_start[nz] = e)
+    uint64_t e_end() const { return pad + e; }
 };
 
 struct DevGraph {
@@ -76,14 +86,24 @@ struct DevGraph {
     std::vector<uint64_t> bounds;          // vertex bounds of every rank (nranks+1)
     std::vector<uint64_t> ebounds;         // edge bounds of every rank
     uint64_t* off = nullptr;
-    uint32_t* src = nullptr;
-    void* w = nullptr;
+    uint32_t* src = nullptr;   // padded: local edge i at src[full.pad + i]
+    void* w = nullptr;         // padded likewise
     gg_weight_kind wkind = GG_W_NONE;
     uint32_t* outdeg = nullptr;
-    TaskList full;
+    ListMeta full;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     Workspace ws;
+    void* h_ctr = nullptr;            // pinned host mirror of the iteration counters
+    cudaEvent_t ev[8] = {};           // timing events, created on first use
+    void* host_counters(size_t bytes) {
+        if (!h_ctr) GGB_CUDA(cudaHostAlloc(&h_ctr, bytes, cudaHostAllocDefault));
+        return h_ctr;
+    }
+    cudaEvent_t event(int i) {
+        if (!ev[i]) GGB_CUDA(cudaEventCreate(&ev[i]));
+        return ev[i];
+    }
     ~DevGraph();
 };
 
@@ -100,12 +120,17 @@ struct RmatCsc {
 RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st);
 void bp_priors_device(uint64_t n, uint64_t seed, float* out, cudaStream_t st);
 
-// Build {window, chunk} work lists for a list with local offsets `off`.
-void build_tasks(DevGraph& g, const uint64_t* off, const std::string& tag, TaskList& out);
-// flags -> sparsified CSC (s_off/s_src/s_w) + its task list. Returns kept edges.
+// Size `meta` for (pad, e) and build its run -> vertex map from `off`.
+void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e,
+                const std::string& tag, ListMeta& meta);
+// flags -> sparsified CSC (s_off, padded s_src/s_w) + its run map. Returns
+// the kept (local) edge count.
 uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
-                        void* s_w, TaskList& out, const std::string& tag,
-                        cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
+                        void* s_w, ListMeta& meta, cudaEvent_t ev0, cudaEvent_t ev1,
+                        int* launches);
+// padded-position base of the sparsified list of this rank (exclusive scan
+// of kept counts over ranks, modulo the task size); 0 on one GPU.
+uint64_t sparse_pad(DevGraph& g, uint64_t kept_local);
 // engine.cpp:63-75 sparsify into a bitmap over local edges (global ids hashed).
 void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones);
 // Deferred superstep bad-vertex scan.

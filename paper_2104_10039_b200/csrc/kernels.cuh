@@ -1,27 +1,34 @@
-// kernels.cuh — the hot path: one fused gather + GG-EStatus + GG-Apply +
-// GG-VStatus kernel per iteration, plus the superstep hub pass.
+// kernels.cuh — the hot path, as an edge-centric gather + a vertex epilogue.
 //
 // Replaces the reference's iteration body (engine.hpp:177-241):
-//   * skip test            engine.hpp:196
-//   * gather fold          engine.hpp:198-213 (GG-Gather, influence inline)
-//   * superstep estatus    engine.hpp:207-211, 214 (GG-EStatus -> bitmap)
-//   * apply/vstatus/valid  engine.hpp:216-224 (GG-Apply, GG-VStatus)
+//   edge_kernel    gather fold (GG-Gather, engine.hpp:198-213) over the
+//                  current list, influence + GG-EStatus into the active-edge
+//                  bitmap during supersteps (engine.hpp:204-211);
+//   vertex_kernel  skip test (:196), GG-Apply / GG-VStatus / valid (:216-224),
+//                  next = prev carry-over (:183), iteration counters;
+//   edge_pass2     superstep flags of edges whose vertex's fold began in an
+//                  earlier task (needs that task's carry).
 //
-// Work decomposition (B200-first, power-law safe):
-//   window  = 32 consecutive destination vertices (aligned), lane k owns
-//             vertex k's accumulator and apply;
-//   row     = 32 consecutive in-edges of the window's list (one per lane,
-//             coalesced 128 B source loads), reduced by a segmented warp scan
-//             keyed by destination;
-//   task    = up to kRowsPerChunk rows of one window = one warp. Windows with
-//             more edges are split into chunks; the last chunk to finish
-//             (atomic ticket) combines the per-chunk partials IN CHUNK ORDER
-//             and applies.
-// Every vertex's fold structure depends only on its window-relative edge
-// positions, so results are bitwise identical for any grid size, any launch
-// order and any 32-aligned multi-GPU partition (the analogue of the
-// reference's thread-count invariance, test_engine.cpp:161-182).
+// Layout (per rank): the list (full or sparsified CSC) is addressed by PADDED
+// positions P = pad + local edge index, with pad chosen so that P equals the
+// global position modulo kChunkEdges; sources/weights are stored at [P].
+//   run  r = padded positions [16r, 16r+16): folded SEQUENTIALLY by one lane
+//            (the reference's inner loop over that stretch); sources come in
+//            as four aligned 128-bit loads, the 16 message gathers are issued
+//            back to back (registers);
+//   task t = runs [32t, 32t+32) = 512 positions = one warp. The task's
+//            non-empty vertices' start offsets are staged in shared memory
+//            (empty vertices are never visited); runs that share a
+//            destination are joined by one segmented warp scan; vertices
+//            that end inside the task get their final accumulator (acc_out),
+//            the task's continuing head / tail pieces go to hv[t] / tv[t] and
+//            are joined in task order by the vertex kernel.
+// Every vertex's fold structure is therefore a function of global edge
+// positions only: results are bitwise identical for any grid, launch order
+// and GPU count (the analogue of test_engine.cpp:161-182).
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -46,349 +53,368 @@ struct IterCounters {
     unsigned int pad;
 };
 
+// edge kernel flavours
+enum : int {
+    kEdgePlain = 0,  // every edge of the list belongs to a processed vertex
+    kEdgeCheck = 1,  // full list, skip edges of unprocessed vertices
+    kEdgeSuper = 2,  // superstep: + influence / estatus into the bitmap
+};
+
+// non-empty vertex starts of one task, relative to the task start, clamped
+// to [-1, 513] (-1: began in an earlier task, 513: ends in a later one)
+constexpr int kStageStarts = kChunkEdges + 2;
+
 template <class P, class W>
-struct IterArgs {
+struct EdgeArgs {
     P prog;
-    uint64_t n;                 // global vertex count
-    uint32_t v_begin;           // first owned vertex (multiple of 32)
-    uint32_t nloc;              // owned vertices
-    // gather list (full CSC or sparsified CSC), local vertex / edge ids
-    const uint64_t* __restrict__ g_off;
-    const uint32_t* __restrict__ g_src;
-    const W* __restrict__ g_w;
-    const uint4* __restrict__ tasks;   // {window, chunk, nchunks, partial slot of chunk 0}
-    uint32_t ntasks;
-    // active_in_degree source (engine.hpp:154-161, :214): offsets of the
-    // current flag set (full CSC offsets under the accurate scheme)
+    const uint32_t* __restrict__ src;       // [padded position]
+    const W* __restrict__ w;                // [padded position]
+    const uint32_t* __restrict__ run_i;     // [run] non-empty vertex at its first position
+    const uint32_t* __restrict__ nz_vid;    // [nz] local vertex id
+    const uint64_t* __restrict__ nz_start;  // [nz+1] local edge offset
+    uint64_t pad, e_end;                    // valid padded positions [pad, e_end)
+    uint64_t ntasks, nruns, nz;
+    const uint64_t* __restrict__ a_off;     // active_in_degree offsets (engine.hpp:154-161)
+    const uint8_t* __restrict__ st_cur;
+    const typename P::Message* __restrict__ msg_cur;  // global ids
+    uint32_t hot_limit;                     // sources below this id: L2 evict_last
+    typename P::Accum* __restrict__ acc_out;  // [local vertex]
+    typename P::Accum* __restrict__ hv;       // [task] continuing head piece
+    typename P::Accum* __restrict__ tv;       // [task] continuing tail piece
+    const typename P::Accum* __restrict__ carry;  // [task] pass 2: carry into the task
+    uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
+    double theta;
+};
+
+template <class P, class W>
+struct VertexArgs {
+    P prog;
+    uint64_t n;
+    uint32_t v_begin, nloc;
+    const uint64_t* __restrict__ off;   // list offsets (unpadded)
+    uint64_t pad;
     const uint64_t* __restrict__ a_off;
     const uint8_t* __restrict__ st_cur;
     uint8_t* __restrict__ st_next;
-    typename P::Property* __restrict__ prop;          // local ids (unused if kMsgIsProp)
+    typename P::Property* __restrict__ prop;          // local ids (unless kMsgIsProp)
     const typename P::Message* __restrict__ msg_cur;  // global ids
-    typename P::Message* __restrict__ msg_next;       // global ids
+    typename P::Message* __restrict__ msg_next;
     const uint32_t* __restrict__ outdeg;              // global ids
-    uint32_t* __restrict__ bitmap;                    // local full-CSC edge ids
-    double theta;
-    typename P::Accum* __restrict__ partials;         // [multi-chunk tasks][32]
-    uint32_t* __restrict__ win_ticket;                // [windows]
+    const typename P::Accum* __restrict__ acc_out;
+    const typename P::Accum* __restrict__ hv;
+    const typename P::Accum* __restrict__ tv;
+    typename P::Accum* __restrict__ carry;            // superstep: carry into task t
     IterCounters* __restrict__ ctr;
 };
 
-struct WarpCounters {
-    unsigned long long gathered = 0, processed = 0;
-    unsigned int changed = 0, any_invalid = 0, bad_min = 0xffffffffu;
-};
+__device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t v) {
+    return (st[v] & kStActive) || a_off[v + 1] > a_off[v];  // engine.hpp:196
+}
 
-template <class P>
-struct WarpSmem {
-    uint32_t rel[kWindow + 1];                  // window-relative list offsets
-    typename P::Accum part[2][kWindow];         // row partials, double buffered
-};
+template <class W>
+using WStore = std::conditional_t<std::is_void_v<W>, char, W>;
 
-// Fold one row of 32 edges (one per lane) into the owners' accumulators.
-// Returns nothing; `acc` is lane k's accumulator for window vertex k.
-// If SUPER, also evaluates each edge's influence against the exclusive
-// prefix (carry + in-row segmented prefix) and writes the active-edge bitmap.
-template <class P, bool SUPER>
-__device__ __forceinline__ void fold_row(const P& prog, WarpSmem<P>& sm, int lane, int parity,
-                                         bool valid, bool eproc, int key,
-                                         const typename P::Message& m, double w,
-                                         typename P::Accum& acc, double theta,
-                                         uint32_t* bitmap, uint64_t row_e0, bool do_flags) {
-    using Accum = typename P::Accum;
-    Accum x = prog.gather_identity();
-    if (eproc) (void)prog.gather(x, m, w);
-    // inclusive segmented scan (Hillis-Steele) keyed by destination
+// Load this lane's sources (aligned run -> 4 x 128-bit) and issue its
+// message gathers back to back.
+template <class P, class W>
+__device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, uint64_t lo,
+                                         uint64_t hi, typename P::Message (&m)[kRun],
+                                         WStore<W> (&wr)[kRun], uint64_t pol_stream,
+                                         uint64_t pol_hot, uint64_t pol_cold) {
+    uint32_t s[kRun];
+    if (lo == P0 && hi == P0 + kRun) {
+        const uint4* sp = reinterpret_cast<const uint4*>(a.src + P0);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const Accum y = shfl_up_any(x, d);
-        const int ky = __shfl_up_sync(0xffffffffu, key, d);
-        if (lane >= d && ky == key) x = prog.combine(y, x);
+        for (int i = 0; i < kRun / 4; ++i) {
+            uint4 q;
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(sp + i), "l"(pol_stream));
+            s[4 * i] = q.x; s[4 * i + 1] = q.y; s[4 * i + 2] = q.z; s[4 * i + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) {
+            const uint64_t p = P0 + j;
+            s[j] = (p >= lo && p < hi) ? ld_stream_u32(a.src + p, pol_stream) : 0u;
+        }
     }
-    const int knext = __shfl_down_sync(0xffffffffu, key, 1);
-    const bool tail = valid && (lane == 31 || knext != key);
-    if (SUPER && do_flags) {  // warp-uniform
-        const Accum xe_raw = shfl_up_any(x, 1);
-        const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
-        const Accum carry = shfl_idx_any(acc, key & 31);
-        Accum pre = (lane > 0 && kprev == key) ? prog.combine(carry, xe_raw) : carry;
-        double infl = 0.0;
-        if (eproc) infl = prog.gather(pre, m, w);  // GG-Gather influence (engine.hpp:204-206)
-        const bool keep = eproc && prog.estatus(infl, theta);  // GG-EStatus (:208)
-        const uint32_t K = __ballot_sync(0xffffffffu, keep);
-        const uint32_t O = __ballot_sync(0xffffffffu, eproc);
-        if (O != 0 && lane < 2) {
-            const uint32_t sh = (uint32_t)(row_e0 & 31);
-            const uint64_t word0 = row_e0 >> 5;
-            const uint64_t K64 = (uint64_t)K << sh, O64 = (uint64_t)O << sh;
-            const uint32_t o = lane == 0 ? (uint32_t)O64 : (uint32_t)(O64 >> 32);
-            const uint32_t k = lane == 0 ? (uint32_t)K64 : (uint32_t)(K64 >> 32);
-            if (o) {
-                // flags of edges of skipped vertices persist (SPEC: superstep scope)
-                atomicAnd(bitmap + word0 + lane, ~o);
-                atomicOr(bitmap + word0 + lane, k & o);
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+        const uint64_t p = P0 + j;
+        if (p >= lo && p < hi) {
+            m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
+            if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + p);
+        }
+    }
+}
+
+template <class P, class W, int MODE>
+__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint64_t t,
+                                          int lane, bool pass2, uint64_t pol_stream,
+                                          uint64_t pol_hot, uint64_t pol_cold) {
+    using Accum = typename P::Accum;
+    using Message = typename P::Message;
+    constexpr bool SUPER = MODE == kEdgeSuper;
+    const uint64_t tstart = t * kChunkEdges;
+    // non-empty vertices touching the task: [i0, i_next], starts staged
+    const uint32_t i0 = a.run_i[t * kWarp];
+    const uint64_t rn = (t + 1) * kWarp;
+    const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
+    const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
+    for (uint32_t j = lane; j < cnt; j += kWarp) {
+        const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
+        st0[j] = (int16_t)(rel < 0 ? -1 : (rel > kChunkEdges ? kChunkEdges + 1 : rel));
+    }
+    __syncwarp();
+    const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
+    if (pass2 && !cont) return;    // warp-uniform
+    const uint64_t r = t * kWarp + lane;
+    const uint64_t P0 = r * kRun;
+    const uint64_t lo = P0 > a.pad ? P0 : a.pad;
+    const uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
+    const int len = hi > lo ? (int)(hi - lo) : 0;
+    const int rlo = (int)(lo - tstart), rhi = (int)(hi - tstart);  // task-relative
+
+    Message m[kRun];
+    WStore<W> wr[kRun];
+    if (len > 0) load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
+    auto wv = [&](int j) -> double {
+        if constexpr (std::is_void_v<W>) return 1.0;
+        else return (double)wr[j];
+    };
+
+    // sequential fold of the run, closing the vertices that end inside it
+    // (k: index relative to i0; nb: task-relative end of vertex k)
+    int k = len > 0 ? (int)(a.run_i[r] - i0) : 0;
+    const int hk = k;
+    int nb = len > 0 ? st0[k + 1] : 0;
+    bool pk = true;
+    if constexpr (MODE != kEdgePlain)
+        if (len > 0) pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
+    uint32_t pmask = 0;  // edges of processed vertices (flags we own)
+    Accum x = a.prog.gather_identity(), hvv = x;
+    bool head_closed = false;
+#pragma unroll
+    for (int j = 0; j < kRun; ++j) {
+        const int p = (int)(P0 - tstart) + j;
+        if (p >= rlo && p < rhi) {
+            if (p >= nb) {  // vertex k ended before p: next non-empty vertex
+                if (!head_closed) {
+                    hvv = x;
+                    head_closed = true;
+                } else if (!pass2) {
+                    a.acc_out[a.nz_vid[i0 + k]] = x;  // began and ended inside this run
+                }
+                x = a.prog.gather_identity();
+                ++k;
+                nb = st0[k + 1];
+                if constexpr (MODE != kEdgePlain)
+                    pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
+            }
+            if (pk) {
+                (void)a.prog.gather(x, m[j], wv(j));
+                pmask |= 1u << j;
             }
         }
     }
-    if (tail) sm.part[parity][key] = x;
-    const uint32_t have = __reduce_or_sync(0xffffffffu, tail ? (1u << (key & 31)) : 0u);
-    __syncwarp();
-    if ((have >> lane) & 1u) acc = prog.combine(acc, sm.part[parity][lane]);
+    const uint32_t tk = len > 0 ? (uint32_t)k : 0x7fffff00u + (uint32_t)lane;  // unique when empty
+    // join runs sharing a destination: segmented inclusive scan keyed by tk
+    Accum S = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Accum y = shfl_up_any(S, d);
+        const uint32_t ky = __shfl_up_sync(0xffffffffu, tk, d);
+        if (lane >= d && ky == tk) S = a.prog.combine(y, S);
+    }
+    const Accum prevS = shfl_up_any(S, 1);
+    const uint32_t prevK = __shfl_up_sync(0xffffffffu, tk, 1);
+    const bool joins_prev = len > 0 && lane > 0 && prevK == (uint32_t)hk;
+    if (!pass2) {
+        if (head_closed) {
+            const Accum hval = joins_prev ? a.prog.combine(prevS, hvv) : hvv;
+            if (cont && hk == 0) a.hv[t] = hval;
+            else a.acc_out[a.nz_vid[i0 + hk]] = hval;
+        }
+        const int nextLen = __shfl_down_sync(0xffffffffu, len, 1);
+        const uint32_t nextHK = __shfl_down_sync(0xffffffffu, (uint32_t)hk, 1);
+        const bool tail_here = len > 0 && (lane == 31 || nextLen == 0 || nextHK != tk);
+        if (tail_here) {
+            const bool cont_after = nb > rhi;  // the vertex goes on past this task
+            const bool first_cont = cont && tk == 0;
+            if (first_cont) a.hv[t] = S;
+            if (cont_after) a.tv[t] = S;
+            else if (!first_cont) a.acc_out[a.nz_vid[i0 + tk]] = S;
+        }
+    }
+    if constexpr (SUPER) {
+        // influence of each edge against its exclusive running prefix
+        // (engine.hpp:204-211); a vertex whose fold began in an earlier task
+        // is handled by pass 2 with that task's carry.
+        Accum run = a.prog.gather_identity();
+        bool skip_head = false;
+        if (cont && hk == 0) {
+            if (pass2) run = a.carry[t];
+            else skip_head = true;
+        } else if (pass2) {
+            skip_head = true;  // pass 2 only rewrites the continuing vertex
+        }
+        if (joins_prev) run = a.prog.combine(run, prevS);
+        uint32_t kbits = 0, own = pmask;
+        int nb2 = len > 0 ? st0[hk + 1] : 0;
+        int kk = hk;
+        bool in_head = true;
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) {
+            const int p = (int)(P0 - tstart) + j;
+            if (p >= rlo && p < rhi) {
+                if (p >= nb2) {
+                    ++kk;
+                    nb2 = st0[kk + 1];
+                    run = a.prog.gather_identity();
+                    in_head = false;
+                }
+                const bool mine = in_head ? !skip_head : !pass2;
+                if (!mine) {
+                    own &= ~(1u << j);
+                } else if ((pmask >> j) & 1u) {
+                    const double infl = a.prog.gather(run, m[j], wv(j));
+                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
+                }
+            }
+        }
+        if (own) {
+            const uint64_t e0 = lo - a.pad;  // local edge id of bit (lo - P0)
+            const uint32_t shift_in = (uint32_t)(lo - P0);
+            const uint32_t O = own >> shift_in, K = kbits >> shift_in;
+            const uint32_t sh = (uint32_t)(e0 & 31);
+            const uint64_t K64 = (uint64_t)K << sh, O64 = (uint64_t)O << sh;
+            uint32_t* wp = a.bitmap + (e0 >> 5);
+            // flags of edges of skipped vertices persist (SPEC: superstep scope)
+            if ((uint32_t)O64) { atomicAnd(wp, ~(uint32_t)O64); atomicOr(wp, (uint32_t)K64); }
+            if ((uint32_t)(O64 >> 32)) {
+                atomicAnd(wp + 1, ~(uint32_t)(O64 >> 32));
+                atomicOr(wp + 1, (uint32_t)(K64 >> 32));
+            }
+        }
+    }
+    __syncwarp();  // st0 is restaged by the warp's next task
+}
+
+template <class P, class W, int MODE>
+__global__ void __launch_bounds__(kBlockThreads)
+edge_kernel(const EdgeArgs<P, W> a) {
+    __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_hot = policy_evict_last();
+    const uint64_t pol_cold = policy_evict_normal();
+    const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
+    for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
+         t += warps)
+        edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, false, pol_stream, pol_hot,
+                              pol_cold);
 }
 
 template <class P, class W>
-__device__ __forceinline__ void apply_vertex(const IterArgs<P, W>& a, uint32_t lv, bool proc,
-                                             uint8_t st, uint64_t list_deg,
-                                             const typename P::Accum& acc, int mode,
-                                             WarpCounters& wc) {
+__global__ void __launch_bounds__(kBlockThreads)
+edge_pass2_kernel(const EdgeArgs<P, W> a) {
+    __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_hot = policy_evict_last();
+    const uint64_t pol_cold = policy_evict_normal();
+    const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
+    for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
+         t += warps)
+        edge_task<P, W, kEdgeSuper>(a, st_all[threadIdx.x >> 5], t, lane, true, pol_stream,
+                                    pol_hot, pol_cold);
+}
+
+// Vertex epilogue: the accumulator of vertex v is acc_out[v] when its list
+// lies inside one task, else tv[t0] (+) hv[t0+1] (+) ... (+) hv[t1] in task
+// order; then GG-Apply, GG-VStatus, valid, message, status, counters.
+template <class P, class W, bool SUPER>
+__global__ void __launch_bounds__(256)
+vertex_kernel(const VertexArgs<P, W> a) {
+    using Accum = typename P::Accum;
     using Property = typename P::Property;
-    const uint32_t v = a.v_begin + lv;
-    if (proc) {
+    unsigned long long g = 0, pcount = 0;
+    unsigned int changed = 0, inv = 0, bad = 0xffffffffu;
+    for (uint32_t lv = blockIdx.x * blockDim.x + threadIdx.x; lv < a.nloc;
+         lv += gridDim.x * blockDim.x) {
+        const uint32_t v = a.v_begin + lv;
+        const uint8_t st = a.st_cur[lv];
+        const uint64_t o0 = a.off[lv], o1 = a.off[lv + 1];
+        const bool proc = (st & kStActive) || a.a_off[lv + 1] > a.a_off[lv];
         Property prev;
         if constexpr (P::kMsgIsProp) prev = a.msg_cur[v];
         else prev = a.prop[lv];
-        const Property fresh = a.prog.apply(v, acc, prev, a.n);    // GG-Apply (:216)
-        const bool active = a.prog.vstatus(prev, fresh);           // GG-VStatus (:217)
-        const bool ok = a.prog.valid(fresh);                       // (:218)
-        if constexpr (!P::kMsgIsProp) a.prop[lv] = fresh;
-        uint32_t deg = 0;
-        if constexpr (P::kNeedsDegree) deg = a.outdeg[v];
-        a.msg_next[v] = a.prog.message(fresh, deg);
-        a.st_next[lv] = (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
-        wc.gathered += list_deg;
-        wc.processed += 1;
-        wc.changed |= active ? 1u : 0u;
-        if (!ok) {
-            wc.any_invalid = 1;
-            // outside supersteps the reference's scan condition
-            // (status || active_in_degree > 0, engine.hpp:229) is exactly
-            // "processed"; supersteps are re-checked after the rebuild.
-            if (mode != kModeSuperstep) wc.bad_min = min(wc.bad_min, v);
-        }
-    } else {
-        // skipped: next = prev (engine.hpp:183), status 0. The message
-        // buffers only differ if the vertex was processed last iteration.
-        if (st & kStProcessed) a.msg_next[v] = a.msg_cur[v];
-        a.st_next[lv] = 0;
-    }
-}
-
-template <class P, class W, bool SUPER, int U>
-__global__ void __launch_bounds__(kBlockThreads)
-iteration_kernel(const IterArgs<P, W> a) {
-    using Accum = typename P::Accum;
-    using Message = typename P::Message;
-    constexpr int MODE = SUPER ? kModeSuperstep : kModeAccurate;
-    __shared__ WarpSmem<P> smem_all[kWarpsPerBlock];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    WarpSmem<P>& sm = smem_all[wib];
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_keep = policy_evict_last();
-    WarpCounters wc;
-    const uint32_t total_warps = gridDim.x * kWarpsPerBlock;
-
-    for (uint32_t t = blockIdx.x * kWarpsPerBlock + wib; t < a.ntasks; t += total_warps) {
-        const uint4 tk = a.tasks[t];
-        const uint32_t win = tk.x, chunk = tk.y, nch = tk.z, slot0 = tk.w;
-        const uint32_t lv0 = win * kWindow;
-        const uint32_t nv = min((uint32_t)kWindow, a.nloc - lv0);
-        const uint64_t base = a.g_off[lv0];
-        const uint64_t my_off = lane < (int)nv ? a.g_off[lv0 + lane] : 0;
-        const uint64_t wend = a.g_off[lv0 + nv];
-        const uint32_t wedges = (uint32_t)(wend - base);
-        sm.rel[lane] = lane < (int)nv ? (uint32_t)(my_off - base) : wedges;
-        if (lane == 0) sm.rel[32] = wedges;
-        // processed test (engine.hpp:196)
-        uint8_t st = 0;
-        uint64_t aid = 0;
-        if (lane < (int)nv) {
-            st = a.st_cur[lv0 + lane];
-            aid = a.a_off[lv0 + lane + 1] - a.a_off[lv0 + lane];
-        }
-        const bool proc = lane < (int)nv && ((st & kStActive) || aid > 0);
-        const uint32_t proc_mask = __ballot_sync(0xffffffffu, proc);
-        __syncwarp();
-        const uint32_t nrows = (wedges + 31) >> 5;
-        const bool multi = nch > 1;
-        const uint32_t r0 = chunk * kRowsPerChunk;
-        const uint32_t r1 = min(nrows, r0 + kRowsPerChunk);
-
-        Accum acc = a.prog.gather_identity();
-        // initial destination of this lane's first edge: largest k with rel[k] <= p
-        int k = 0;
-        {
-            const uint32_t p = r0 * 32 + lane;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1)
-                if (k + step < (int)nv && sm.rel[k + step] <= p) k += step;
-        }
-        for (uint32_t row = r0; row < r1; row += U) {
-            uint32_t s[U];
-            double wv[U];
-            Message m[U];
-            int key[U];
-            bool val[U], ep[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t p = (row + u) * 32 + lane;
-                val[u] = (row + u) < r1 && p < wedges;
-                while (k + 1 < (int)nv && sm.rel[k + 1] <= p) ++k;
-                key[u] = val[u] ? k : 32;
-                ep[u] = val[u] && ((proc_mask >> k) & 1u);
-                s[u] = ep[u] ? ld_stream_u32(a.g_src + base + p, pol_stream) : 0u;
-                wv[u] = ep[u] ? WeightIO<W>::load(a.g_w, base + p) : 1.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (ep[u]) m[u] = ld_msg(a.msg_cur + s[u], pol_keep);
-                else memset(&m[u], 0, sizeof(Message));
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (row + u < r1)
-                    fold_row<P, SUPER>(a.prog, sm, lane, (row + u) & 1, val[u], ep[u], key[u],
-                                       m[u], wv[u], acc, a.theta, a.bitmap,
-                                       base + (uint64_t)(row + u) * 32, !multi);
-            }
-        }
-        // Multi-chunk windows get their superstep flags from
-        // superstep_hub_kernel, which has the carry of earlier chunks.
-        if (!multi) {
-            if (lane < (int)nv)
-                apply_vertex(a, lv0 + lane, proc, st, (uint64_t)(sm.rel[lane + 1] - sm.rel[lane]),
-                             acc, MODE, wc);
-        } else {
-            a.partials[(uint64_t)(slot0 + chunk) * kWindow + lane] = acc;
-            __threadfence();
-            uint32_t ticket = 0;
-            if (lane == 0) ticket = atomicAdd(a.win_ticket + win, 1u);
-            ticket = __shfl_sync(0xffffffffu, ticket, 0);
-            if (ticket == nch - 1) {
-                __threadfence();
-                const uint64_t first = slot0;
-                Accum run = a.prog.gather_identity();
-                for (uint32_t c = 0; c < nch; ++c) {
-                    const Accum pc = ld_cg_any(a.partials + (first + c) * kWindow + lane);
-                    if constexpr (SUPER) a.partials[(first + c) * kWindow + lane] = run;
-                    run = a.prog.combine(run, pc);
+        if (proc) {
+            Accum acc = a.prog.gather_identity();
+            if (o1 > o0) {
+                const uint64_t t0 = (o0 + a.pad) / kChunkEdges, t1 = (o1 - 1 + a.pad) / kChunkEdges;
+                if (t0 == t1) {
+                    acc = a.acc_out[lv];
+                } else {
+                    acc = a.tv[t0];
+                    for (uint64_t t = t0 + 1; t <= t1; ++t) {
+                        if constexpr (SUPER) a.carry[t] = acc;
+                        acc = a.prog.combine(acc, a.hv[t]);
+                    }
                 }
-                if (lane == 0) a.win_ticket[win] = 0;
-                if (lane < (int)nv)
-                    apply_vertex(a, lv0 + lane, proc, st,
-                                 (uint64_t)(sm.rel[lane + 1] - sm.rel[lane]), run, MODE, wc);
             }
+            const Property fresh = a.prog.apply(v, acc, prev, a.n);  // GG-Apply (:216)
+            const bool active = a.prog.vstatus(prev, fresh);         // GG-VStatus (:217)
+            const bool ok = a.prog.valid(fresh);                     // (:218)
+            if constexpr (!P::kMsgIsProp) a.prop[lv] = fresh;
+            uint32_t deg = 0;
+            if constexpr (P::kNeedsDegree) deg = a.outdeg[v];
+            a.msg_next[v] = a.prog.message(fresh, deg);
+            a.st_next[lv] = (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
+            g += o1 - o0;
+            pcount += 1;
+            changed |= active ? 1u : 0u;
+            if (!ok) {
+                inv = 1;
+                // outside supersteps the reference's scan condition
+                // (status || active_in_degree > 0, engine.hpp:229) is exactly
+                // "processed"; supersteps are re-checked after the rebuild.
+                if (!SUPER) bad = min(bad, v);
+            }
+        } else {
+            // skipped: next = prev (engine.hpp:183), status 0. The message
+            // buffers only differ if the vertex was processed last iteration.
+            if (st & kStProcessed) {
+                if constexpr (P::kMsgIsProp) a.msg_next[v] = prev;
+                else a.msg_next[v] = a.msg_cur[v];
+            }
+            a.st_next[lv] = 0;
         }
-        __syncwarp();
     }
-
-    // block-level counter aggregation, one atomic per counter per block
-    __shared__ unsigned long long s_g[kWarpsPerBlock], s_p[kWarpsPerBlock];
-    __shared__ unsigned int s_c[kWarpsPerBlock], s_i[kWarpsPerBlock], s_b[kWarpsPerBlock];
+    // block reduction, one atomic per counter per block
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
-        wc.gathered += __shfl_down_sync(0xffffffffu, wc.gathered, d);
-        wc.processed += __shfl_down_sync(0xffffffffu, wc.processed, d);
+        g += __shfl_down_sync(0xffffffffu, g, d);
+        pcount += __shfl_down_sync(0xffffffffu, pcount, d);
     }
-    wc.changed = __reduce_or_sync(0xffffffffu, wc.changed);
-    wc.any_invalid = __reduce_or_sync(0xffffffffu, wc.any_invalid);
-    wc.bad_min = __reduce_min_sync(0xffffffffu, wc.bad_min);
-    if (lane == 0) {
-        s_g[wib] = wc.gathered; s_p[wib] = wc.processed; s_c[wib] = wc.changed;
-        s_i[wib] = wc.any_invalid; s_b[wib] = wc.bad_min;
-    }
+    changed = __reduce_or_sync(0xffffffffu, changed);
+    inv = __reduce_or_sync(0xffffffffu, inv);
+    bad = __reduce_min_sync(0xffffffffu, bad);
+    __shared__ unsigned long long s_g[8], s_p[8];
+    __shared__ unsigned int s_c[8], s_i[8], s_b[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    if (lane == 0) { s_g[wib] = g; s_p[wib] = pcount; s_c[wib] = changed; s_i[wib] = inv; s_b[wib] = bad; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long g = 0, p = 0;
-        unsigned int c = 0, inv = 0, b = 0xffffffffu;
-        for (int i = 0; i < kWarpsPerBlock; ++i) {
-            g += s_g[i]; p += s_p[i]; c |= s_c[i]; inv |= s_i[i]; b = min(b, s_b[i]);
+        const int nw = blockDim.x / 32;
+        for (int i = 1; i < nw; ++i) {
+            g += s_g[i]; pcount += s_p[i]; changed |= s_c[i]; inv |= s_i[i]; bad = min(bad, s_b[i]);
         }
         if (g) atomicAdd(&a.ctr->gathered, g);
-        if (p) atomicAdd(&a.ctr->processed, p);
-        if (c) atomicOr(&a.ctr->changed, c);
+        if (pcount) atomicAdd(&a.ctr->processed, pcount);
+        if (changed) atomicOr(&a.ctr->changed, changed);
         if (inv) atomicOr(&a.ctr->any_invalid, inv);
-        if (b != 0xffffffffu) atomicMin(&a.ctr->bad_min, b);
-    }
-}
-
-// Superstep pass for windows split into several chunks: re-walks their rows
-// with the exclusive chunk carry (written by the last chunk of
-// iteration_kernel) to evaluate each edge's influence against its exact
-// running-fold prefix and rewrite the bitmap.
-template <class P, class W, int U>
-__global__ void __launch_bounds__(kBlockThreads)
-superstep_hub_kernel(const IterArgs<P, W> a, const uint4* __restrict__ mtasks, uint32_t nmtasks) {
-    using Accum = typename P::Accum;
-    using Message = typename P::Message;
-    __shared__ WarpSmem<P> smem_all[kWarpsPerBlock];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    WarpSmem<P>& sm = smem_all[wib];
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_keep = policy_evict_last();
-    const uint32_t total_warps = gridDim.x * kWarpsPerBlock;
-    for (uint32_t i = blockIdx.x * kWarpsPerBlock + wib; i < nmtasks; i += total_warps) {
-        const uint4 tk = mtasks[i];
-        const uint32_t win = tk.x, chunk = tk.y, slot0 = tk.w;
-        const uint32_t lv0 = win * kWindow;
-        const uint32_t nv = min((uint32_t)kWindow, a.nloc - lv0);
-        const uint64_t base = a.g_off[lv0];
-        const uint64_t my_off = lane < (int)nv ? a.g_off[lv0 + lane] : 0;
-        const uint64_t wend = a.g_off[lv0 + nv];
-        const uint32_t wedges = (uint32_t)(wend - base);
-        sm.rel[lane] = lane < (int)nv ? (uint32_t)(my_off - base) : wedges;
-        if (lane == 0) sm.rel[32] = wedges;
-        uint8_t st = 0;
-        uint64_t aid = 0;
-        if (lane < (int)nv) {
-            st = a.st_cur[lv0 + lane];
-            aid = a.a_off[lv0 + lane + 1] - a.a_off[lv0 + lane];
-        }
-        const bool proc = lane < (int)nv && ((st & kStActive) || aid > 0);
-        const uint32_t proc_mask = __ballot_sync(0xffffffffu, proc);
-        __syncwarp();
-        const uint32_t nrows = (wedges + 31) >> 5;
-        const uint32_t r0 = chunk * kRowsPerChunk;
-        const uint32_t r1 = min(nrows, r0 + kRowsPerChunk);
-        Accum acc = a.partials[(uint64_t)(slot0 + chunk) * kWindow + lane];  // exclusive chunk carry
-        int k = 0;
-        {
-            const uint32_t p = r0 * 32 + lane;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1)
-                if (k + step < (int)nv && sm.rel[k + step] <= p) k += step;
-        }
-        for (uint32_t row = r0; row < r1; row += U) {
-            uint32_t s[U];
-            double wv[U];
-            Message m[U];
-            int key[U];
-            bool val[U], ep[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t p = (row + u) * 32 + lane;
-                val[u] = (row + u) < r1 && p < wedges;
-                while (k + 1 < (int)nv && sm.rel[k + 1] <= p) ++k;
-                key[u] = val[u] ? k : 32;
-                ep[u] = val[u] && ((proc_mask >> k) & 1u);
-                s[u] = ep[u] ? ld_stream_u32(a.g_src + base + p, pol_stream) : 0u;
-                wv[u] = ep[u] ? WeightIO<W>::load(a.g_w, base + p) : 1.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (ep[u]) m[u] = ld_msg(a.msg_cur + s[u], pol_keep);
-                else memset(&m[u], 0, sizeof(Message));
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (row + u < r1)
-                    fold_row<P, true>(a.prog, sm, lane, (row + u) & 1, val[u], ep[u], key[u], m[u],
-                                      wv[u], acc, a.theta, a.bitmap,
-                                      base + (uint64_t)(row + u) * 32, true);
-            }
-        }
-        __syncwarp();
+        if (bad != 0xffffffffu) atomicMin(&a.ctr->bad_min, bad);
     }
 }
 

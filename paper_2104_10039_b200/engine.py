@@ -277,6 +277,10 @@ class IterationRecord:
     rebuild_ms: float = 0.0
     exchange_ms: float = 0.0
     algo_bytes: int = 0
+    edge_ms: float = 0.0
+    vertex_ms: float = 0.0
+    edge_bytes: int = 0
+    vertex_bytes: int = 0
 
 
 @dataclass
@@ -383,7 +387,9 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         per = [IterationRecord(IterationMode(recs[i].mode), int(recs[i].processed_edges),
                                int(recs[i].active_vertices), float(recs[i].wall_seconds),
                                float(recs[i].kernel_ms), float(recs[i].rebuild_ms),
-                               float(recs[i].exchange_ms), int(recs[i].algo_bytes))
+                               float(recs[i].exchange_ms), int(recs[i].algo_bytes),
+                               float(recs[i].edge_ms), float(recs[i].vertex_ms),
+                               int(recs[i].edge_bytes), int(recs[i].vertex_bytes))
                for i in range(k)]
         out_props = None if device_output else (props if n else props[:0])
         return RunReport(out_props, int(summ.iterations_run), per,

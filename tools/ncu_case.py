@@ -1,5 +1,5 @@
-"""Small, fixed engine run for ncu captures (one gg run of a BASELINE
-workload; the first iterations are approximate, then a superstep)."""
+"""Small, fixed engine run for timing / ncu captures (one gg run of a
+BASELINE workload; the first iterations are approximate, then a superstep)."""
 import argparse
 import os
 import sys
@@ -12,12 +12,17 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2")
 ap.add_argument("--iters", type=int, default=6)
 ap.add_argument("--scheme", default="gg")
+ap.add_argument("--repeat", type=int, default=1)
 a = ap.parse_args()
 wl = WORKLOADS[a.workload]
 dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"], weights=wl["weights"])
 prog = make_program(ggb, wl, dg, dg.n)
-r = ggb.run(dg, prog, ggb.EngineConfig(a.scheme, SIGMA, wl["theta"], ALPHA, a.iters, wl["seed"]),
-            timing=True, device_output=True)
+for _ in range(a.repeat):
+    r = ggb.run(dg, prog, ggb.EngineConfig(a.scheme, SIGMA, wl["theta"], ALPHA, a.iters, wl["seed"]),
+                timing=True, device_output=True)
+print(f"{a.workload}: run wall {r.total_wall_seconds * 1e3:.2f} ms, {r.kernel_launches} launches")
 for it in r.per_iteration:
-    print(it.mode.name, it.processed_edges, f"{it.kernel_ms:.3f} ms",
-          f"{it.algo_bytes / it.kernel_ms / 1e6:.1f} GB/s" if it.kernel_ms else "")
+    gb = lambda b, ms: f"{b / ms / 1e6:7.1f} GB/s" if ms else "      -"
+    print(f"{it.mode.name:11s} E={it.processed_edges:11d} edge {it.edge_ms:7.3f} ms {gb(it.edge_bytes, it.edge_ms)} "
+          f"| vertex {it.vertex_ms:6.3f} ms {gb(it.vertex_bytes, it.vertex_ms)} | rebuild {it.rebuild_ms:6.3f} "
+          f"| wall {it.wall_seconds * 1e3:7.3f} ms")
