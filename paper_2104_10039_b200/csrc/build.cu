@@ -239,6 +239,92 @@ uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, ui
     return kept;
 }
 
+// --------------------------------------------------------------------------
+// hot-first message slots
+// --------------------------------------------------------------------------
+__global__ void slot_key_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
+                                const uint64_t* __restrict__ bounds, int nranks,
+                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t r = 0;
+        while (r + 1 < (uint64_t)nranks && v >= bounds[r + 1]) ++r;
+        keys[v] = (r << 32) | (uint64_t)(0xffffffffu - outdeg[v]);  // rank, then out-degree desc
+        vals[v] = (uint32_t)v;
+    }
+}
+
+__global__ void slot_fill_kernel(const uint32_t* __restrict__ sorted_v, uint64_t n,
+                                 uint32_t* __restrict__ slot_of, uint32_t* __restrict__ vtx_of_slot) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = sorted_v[i];
+        slot_of[v] = (uint32_t)i;
+        vtx_of_slot[i] = v;
+    }
+}
+
+__global__ void relabel_kernel(uint32_t* __restrict__ src, uint64_t count,
+                               const uint32_t* __restrict__ slot_of) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        src[i] = __ldg(slot_of + src[i]);
+}
+
+void assign_slots(DevGraph& g) {
+    const uint64_t n = g.n;
+    GGB_CUDA(cudaMalloc(&g.slot_of, (n + 1) * 4));
+    GGB_CUDA(cudaMalloc(&g.vtx_of_slot, (n + 1) * 4));
+    if (n == 0) return;
+    uint64_t *k0 = nullptr, *k1 = nullptr, *db = nullptr;
+    uint32_t *v0 = nullptr, *v1 = nullptr;
+    GGB_CUDA(cudaMalloc(&k0, n * 8));
+    GGB_CUDA(cudaMalloc(&k1, n * 8));
+    GGB_CUDA(cudaMalloc(&v0, n * 4));
+    GGB_CUDA(cudaMalloc(&v1, n * 4));
+    GGB_CUDA(cudaMalloc(&db, g.bounds.size() * 8));
+    GGB_CUDA(cudaMemcpyAsync(db, g.bounds.data(), g.bounds.size() * 8, cudaMemcpyHostToDevice,
+                             g.stream));
+    slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, k0, v0);
+    GGB_CUDA(cudaGetLastError());
+    int rank_bits = 0;
+    while ((1 << rank_bits) < g.nranks) ++rank_bits;
+    size_t tmp = 0;
+    GGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
+                                             g.stream));
+    void* tmpp = nullptr;
+    GGB_CUDA(cudaMalloc(&tmpp, tmp));
+    GGB_CUDA(cub::DeviceRadixSort::SortPairs(tmpp, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
+                                             g.stream));
+    slot_fill_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(v1, n, g.slot_of, g.vtx_of_slot);
+    GGB_CUDA(cudaGetLastError());
+    if (g.e_loc) {
+        relabel_kernel<<<grid_for(g.e_loc, 256), 256, 0, g.stream>>>(g.src + g.full.pad, g.e_loc,
+                                                                      g.slot_of);
+        GGB_CUDA(cudaGetLastError());
+    }
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1); cudaFree(db); cudaFree(tmpp);
+}
+
+__global__ void unlabel_kernel(const uint32_t* __restrict__ src, uint64_t count,
+                               const uint32_t* __restrict__ vtx_of_slot, uint32_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = __ldg(vtx_of_slot + src[i]);
+}
+
+void export_sources(const DevGraph& g, uint32_t* host_out) {
+    uint32_t* tmp = nullptr;
+    GGB_CUDA(cudaMalloc(&tmp, (g.e_loc + 1) * 4));
+    unlabel_kernel<<<grid_for(g.e_loc, 256), 256, 0, g.stream>>>(g.src + g.full.pad, g.e_loc,
+                                                                  g.vtx_of_slot, tmp);
+    GGB_CUDA(cudaGetLastError());
+    GGB_CUDA(cudaMemcpyAsync(host_out, tmp, g.e_loc * 4, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    cudaFree(tmp);
+}
+
 __global__ void superstep_invalid_kernel(uint32_t nloc, uint32_t v_begin,
                                          const uint8_t* __restrict__ st_cur,
                                          const uint8_t* __restrict__ st_next,
@@ -267,6 +353,8 @@ DevGraph::~DevGraph() {
     if (src) cudaFree(src);
     if (w) cudaFree(w);
     if (outdeg) cudaFree(outdeg);
+    if (slot_of) cudaFree(slot_of);
+    if (vtx_of_slot) cudaFree(vtx_of_slot);
     if (stream) cudaStreamDestroy(stream);
 }
 

@@ -155,6 +155,7 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                                              g.stream));
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
             }
+            assign_slots(g);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
@@ -207,6 +208,7 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
                 cudaFree(r.src);
                 if (r.w) cudaFree(r.w);
             }
+            assign_slots(g);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
@@ -249,7 +251,7 @@ gg_status gg_dev_graph_export(const gg_dev_graph* h, uint64_t* offsets, uint32_t
         GGB_CUDA(cudaSetDevice(g.device));
         if (offsets) GGB_CUDA(cudaMemcpy(offsets, g.off, (g.nloc + 1) * 8, cudaMemcpyDeviceToHost));
         if (sources && g.e_loc)
-            GGB_CUDA(cudaMemcpy(sources, g.src + g.full.pad, g.e_loc * 4, cudaMemcpyDeviceToHost));
+            export_sources(g, sources);  // slot ids back to vertex ids
         const size_t wb = weight_size(g.wkind);
         if (weights && wb && g.e_loc)
             GGB_CUDA(cudaMemcpy(weights, static_cast<const char*>(g.w) + g.full.pad * wb,

@@ -51,6 +51,7 @@ struct RunIO {
 template <class P>
 __global__ void init_kernel(P prog, uint64_t n, uint32_t v_begin, uint32_t nloc,
                             const uint32_t* __restrict__ outdeg,
+                            const uint32_t* __restrict__ slot_of,
                             typename P::Message* __restrict__ msg,
                             typename P::Property* __restrict__ prop, uint8_t* __restrict__ st) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
@@ -58,9 +59,9 @@ __global__ void init_kernel(P prog, uint64_t n, uint32_t v_begin, uint32_t nloc,
         const typename P::Property p = prog.init_property((uint32_t)v, n);  // engine.hpp:164
         uint32_t deg = 0;
         if constexpr (P::kNeedsDegree) deg = outdeg[v];
-        msg[v] = prog.message(p, deg);
+        msg[slot_of[v]] = prog.message(p, deg);
         if (v >= v_begin && v < (uint64_t)v_begin + nloc) {
-            if constexpr (!P::kMsgIsProp) prop[v - v_begin] = p;
+            prop[v - v_begin] = p;
             st[v - v_begin] = kStActive;  // status starts at 1 (engine.hpp:166)
         }
     }
@@ -135,7 +136,7 @@ struct Engine {
         Workspace& ws = g.ws;
 
         Msg* msg[2] = {ws.get<Msg>("msg0", n), ws.get<Msg>("msg1", n)};
-        Prop* prop = P::kMsgIsProp ? nullptr : ws.get<Prop>("prop", nloc);
+        Prop* prop = ws.get<Prop>("prop", nloc + 1);
         uint8_t* st[2] = {ws.get<uint8_t>("st0", nloc + 1), ws.get<uint8_t>("st1", nloc + 1)};
         IterCounters* ctr = ws.get<IterCounters>("ctr", 1);
         IterCounters* h_ctr = static_cast<IterCounters*>(g.host_counters(sizeof(IterCounters)));
@@ -157,8 +158,8 @@ struct Engine {
         cudaEvent_t e6 = timing ? g.event(6) : nullptr, e7 = timing ? g.event(7) : nullptr;
 
         init_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, n, (uint32_t)g.v_begin,
-                                                         (uint32_t)nloc, g.outdeg, msg[0], prop,
-                                                         st[0]);
+                                                         (uint32_t)nloc, g.outdeg, g.slot_of, msg[0],
+                                                         prop, st[0]);
         GGB_CUDA(cudaGetLastError());
         ++launches;
         uint64_t kept = g.e_loc;
@@ -172,7 +173,11 @@ struct Engine {
             kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches);
         }
         const uint64_t* a_off = sparse ? s_off : g.off;
-        const uint32_t hot_limit = (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg));
+        // the hottest message slots (lowest ids: hot-first layout) are pinned in
+        // L2 with evict_last; with several ranks each range has its own hot
+        // prefix and every gather uses evict_normal.
+        const uint32_t hot_limit =
+            g.nranks == 1 ? (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg)) : 0u;
 
         int cur = 0;
         uint64_t iterations_run = 0, total_edges = 0;
@@ -219,6 +224,7 @@ struct Engine {
             va.msg_cur = msg[cur];
             va.msg_next = msg[cur ^ 1];
             va.outdeg = g.outdeg;
+            va.slot_of = g.slot_of;
             va.acc_out = acc_out;
             va.hv = hv;
             va.tv = tv;
@@ -311,15 +317,11 @@ struct Engine {
         }
 
         // final properties (engine.hpp:243)
-        Prop* final_all;
-        if constexpr (P::kMsgIsProp) {
-            final_all = msg[cur];  // exchanged every iteration: full on every rank
-        } else {
-            final_all = ws.get<Prop>("final", n);
-            GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
-                                     cudaMemcpyDeviceToDevice, g.stream));
-            if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
-        }
+        // owned properties (vertex order) gathered from every rank
+        Prop* final_all = ws.get<Prop>("final", n);
+        GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
+                                 cudaMemcpyDeviceToDevice, g.stream));
+        if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
         if (io.out_props && !(io.opts && io.opts->device_output)) {
             if constexpr (requires { P::kRawOutput; }) {  // WCC: uint32 labels as-is
                 GGB_CUDA(cudaMemcpyAsync(io.out_props, final_all, n * 4, cudaMemcpyDeviceToHost,

@@ -90,6 +90,11 @@ struct DevGraph {
     void* w = nullptr;         // padded likewise
     gg_weight_kind wkind = GG_W_NONE;
     uint32_t* outdeg = nullptr;
+    // Message-slot layout: messages are stored hot-first (descending
+    // out-degree within each rank's range) so the gathers' hot set packs
+    // into L2; src arrays hold slot ids. slot_of[v] / vtx_of_slot[s], global.
+    uint32_t* slot_of = nullptr;
+    uint32_t* vtx_of_slot = nullptr;
     ListMeta full;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
@@ -120,6 +125,11 @@ struct RmatCsc {
 RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st);
 void bp_priors_device(uint64_t n, uint64_t seed, float* out, cudaStream_t st);
 
+// Hot-first message slots (slot_of / vtx_of_slot) and the rewrite of the
+// full list's sources from vertex ids to slot ids.
+void assign_slots(DevGraph& g);
+// Copy the full list's sources back to host as vertex ids.
+void export_sources(const DevGraph& g, uint32_t* host_out);
 // Size `meta` for (pad, e) and build its run -> vertex map from `off`.
 void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e,
                 const std::string& tag, ListMeta& meta);

@@ -96,10 +96,11 @@ struct VertexArgs {
     const uint64_t* __restrict__ a_off;
     const uint8_t* __restrict__ st_cur;
     uint8_t* __restrict__ st_next;
-    typename P::Property* __restrict__ prop;          // local ids (unless kMsgIsProp)
-    const typename P::Message* __restrict__ msg_cur;  // global ids
+    typename P::Property* __restrict__ prop;          // local vertex ids
+    const typename P::Message* __restrict__ msg_cur;  // message slots
     typename P::Message* __restrict__ msg_next;
     const uint32_t* __restrict__ outdeg;              // global ids
+    const uint32_t* __restrict__ slot_of;             // global id -> message slot
     const typename P::Accum* __restrict__ acc_out;
     const typename P::Accum* __restrict__ hv;
     const typename P::Accum* __restrict__ tv;
@@ -343,12 +344,11 @@ vertex_kernel(const VertexArgs<P, W> a) {
     for (uint32_t lv = blockIdx.x * blockDim.x + threadIdx.x; lv < a.nloc;
          lv += gridDim.x * blockDim.x) {
         const uint32_t v = a.v_begin + lv;
+        const uint32_t sv = a.slot_of[v];
         const uint8_t st = a.st_cur[lv];
         const uint64_t o0 = a.off[lv], o1 = a.off[lv + 1];
         const bool proc = (st & kStActive) || a.a_off[lv + 1] > a.a_off[lv];
-        Property prev;
-        if constexpr (P::kMsgIsProp) prev = a.msg_cur[v];
-        else prev = a.prop[lv];
+        const Property prev = a.prop[lv];
         if (proc) {
             Accum acc = a.prog.gather_identity();
             if (o1 > o0) {
@@ -366,10 +366,10 @@ vertex_kernel(const VertexArgs<P, W> a) {
             const Property fresh = a.prog.apply(v, acc, prev, a.n);  // GG-Apply (:216)
             const bool active = a.prog.vstatus(prev, fresh);         // GG-VStatus (:217)
             const bool ok = a.prog.valid(fresh);                     // (:218)
-            if constexpr (!P::kMsgIsProp) a.prop[lv] = fresh;
+            a.prop[lv] = fresh;
             uint32_t deg = 0;
             if constexpr (P::kNeedsDegree) deg = a.outdeg[v];
-            a.msg_next[v] = a.prog.message(fresh, deg);
+            a.msg_next[sv] = a.prog.message(fresh, deg);
             a.st_next[lv] = (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
             g += o1 - o0;
             pcount += 1;
@@ -384,10 +384,7 @@ vertex_kernel(const VertexArgs<P, W> a) {
         } else {
             // skipped: next = prev (engine.hpp:183), status 0. The message
             // buffers only differ if the vertex was processed last iteration.
-            if (st & kStProcessed) {
-                if constexpr (P::kMsgIsProp) a.msg_next[v] = prev;
-                else a.msg_next[v] = a.msg_cur[v];
-            }
+            if (st & kStProcessed) a.msg_next[sv] = a.msg_cur[sv];
             a.st_next[lv] = 0;
         }
     }
