@@ -6,7 +6,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libggb.so")
+LIB_PATH = os.environ.get("GGB_LIB_PATH", os.path.join(HERE, "libggb.so"))  # override: A/B builds
 
 GG_OK, GG_INVALID_ARGUMENT, GG_INVALID_PROPERTY, GG_CUDA, GG_NCCL, GG_OOM, GG_INTERNAL = range(7)
 GG_W_NONE, GG_W_U32, GG_W_F32, GG_W_F64 = range(4)

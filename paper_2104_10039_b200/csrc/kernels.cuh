@@ -149,9 +149,9 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
     }
 }
 
-template <class P, class W, int MODE>
+template <class P, class W, int MODE, bool PASS2>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint64_t t,
-                                          int lane, bool pass2, uint64_t pol_stream,
+                                          int lane, uint64_t pol_stream,
                                           uint64_t pol_hot, uint64_t pol_cold) {
     using Accum = typename P::Accum;
     using Message = typename P::Message;
@@ -168,11 +168,15 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     }
     __syncwarp();
     const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
-    if (pass2 && !cont) return;    // warp-uniform
+    if (PASS2 && !cont) return;    // warp-uniform
     const uint64_t r = t * kWarp + lane;
     const uint64_t P0 = r * kRun;
     const uint64_t lo = P0 > a.pad ? P0 : a.pad;
-    const uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
+    uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
+    if constexpr (PASS2) {  // pass 2 only re-walks the continuing first vertex's edges
+        const uint64_t vend = tstart + (uint64_t)(st0[1] > 0 ? st0[1] : 0);
+        if (hi > vend) hi = vend;
+    }
     const int len = hi > lo ? (int)(hi - lo) : 0;
     const int rlo = (int)(lo - tstart), rhi = (int)(hi - tstart);  // task-relative
 
@@ -203,7 +207,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 if (!head_closed) {
                     hvv = x;
                     head_closed = true;
-                } else if (!pass2) {
+                } else if (!PASS2) {
                     a.acc_out[a.nz_vid[i0 + k]] = x;  // began and ended inside this run
                 }
                 x = a.prog.gather_identity();
@@ -230,7 +234,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     const Accum prevS = shfl_up_any(S, 1);
     const uint32_t prevK = __shfl_up_sync(0xffffffffu, tk, 1);
     const bool joins_prev = len > 0 && lane > 0 && prevK == (uint32_t)hk;
-    if (!pass2) {
+    if (!PASS2) {
         if (head_closed) {
             const Accum hval = joins_prev ? a.prog.combine(prevS, hvv) : hvv;
             if (cont && hk == 0) a.hv[t] = hval;
@@ -254,9 +258,9 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         Accum run = a.prog.gather_identity();
         bool skip_head = false;
         if (cont && hk == 0) {
-            if (pass2) run = a.carry[t];
+            if (PASS2) run = a.carry[t];
             else skip_head = true;
-        } else if (pass2) {
+        } else if (PASS2) {
             skip_head = true;  // pass 2 only rewrites the continuing vertex
         }
         if (joins_prev) run = a.prog.combine(run, prevS);
@@ -274,7 +278,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     run = a.prog.gather_identity();
                     in_head = false;
                 }
-                const bool mine = in_head ? !skip_head : !pass2;
+                const bool mine = in_head ? !skip_head : !PASS2;
                 if (!mine) {
                     own &= ~(1u << j);
                 } else if ((pmask >> j) & 1u) {
@@ -312,7 +316,7 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
-        edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, false, pol_stream, pol_hot,
+        edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
                               pol_cold);
 }
 
@@ -327,7 +331,7 @@ edge_pass2_kernel(const EdgeArgs<P, W> a) {
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
-        edge_task<P, W, kEdgeSuper>(a, st_all[threadIdx.x >> 5], t, lane, true, pol_stream,
+        edge_task<P, W, kEdgeSuper, true>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream,
                                     pol_hot, pol_cold);
 }
 
