@@ -735,6 +735,68 @@ int og_run(const og_graph* g, int which, const og_params* params,
     return OG_OK;
 }
 
+/* engine.hpp:163-164 */
+int og_init_props(const og_graph* g, int which, const og_params* params, void* out) {
+    int counter = 0;
+    prog P;
+    if (make_prog(which, params, g->n, &counter, &P)) return OG_INVALID_ARGUMENT;
+    for (uint64_t v = 0; v < g->n; ++v) P.init(&P, (uint32_t)v, (uint8_t*)out + v * P.psize);
+    return OG_OK;
+}
+
+/* engine.hpp:194-224 over one destination range, plus the owned part of the
+ * :226-233 scan. Sequential per vertex exactly like og_run. */
+int og_step_range(const og_graph* g, int which, const og_params* params, int mode, double theta,
+                  uint8_t* flags, uint32_t* aid, const void* prev_v, const uint8_t* status,
+                  void* next_v, uint8_t* status_next, uint64_t v_begin, uint64_t v_end,
+                  uint64_t counters[4]) {
+    int counter = 0;
+    prog P;
+    if (make_prog(which, params, g->n, &counter, &P)) return OG_INVALID_ARGUMENT;
+    const size_t ps = P.psize;
+    const uint8_t* prev = (const uint8_t*)prev_v;
+    uint8_t* next = (uint8_t*)next_v;
+    const int approx = mode == OG_MODE_APPROXIMATE, superstep = mode == OG_MODE_SUPERSTEP;
+    uint8_t acc[64], fresh[64];
+    uint64_t gathered = 0, processed = 0, changed = 0;
+    int any_bad = 0;
+    for (uint64_t v = v_begin; v < v_end; ++v) {
+        memcpy(next + v * ps, prev + v * ps, ps);                  /* :183 */
+        status_next[v] = 0;
+        if (!status[v] && aid[v] == 0) continue;                   /* :196 */
+        P.identity(&P, acc);
+        uint64_t local_edges = 0;
+        uint32_t new_active = 0;
+        for (uint64_t e = g->off[v]; e < g->off[v + 1]; ++e) {
+            if (approx && !flags[e]) continue;
+            const uint32_t s = g->src[e];
+            const double w = g->w ? g->w[e] : 1.0;
+            const double infl = P.gather(&P, acc, prev + (uint64_t)s * ps, w, g->outdeg[s]);
+            if (superstep) {
+                const int keep = estatus(infl, theta);
+                flags[e] = keep ? 1 : 0;
+                new_active += keep ? 1 : 0;
+            }
+            ++local_edges;
+        }
+        if (superstep) aid[v] = new_active;
+        P.apply(&P, (uint32_t)v, acc, prev + v * ps, fresh);
+        const int active = P.vstatus(&P, prev + v * ps, fresh);
+        if (!P.valid(&P, fresh)) any_bad = 1;
+        memcpy(next + v * ps, fresh, ps);
+        status_next[v] = active ? 1 : 0;
+        changed |= active ? 1u : 0u;
+        gathered += local_edges;
+        ++processed;
+    }
+    uint64_t bad = 0;
+    if (any_bad)
+        for (uint64_t v = v_begin; v < v_end && !bad; ++v)
+            if ((status[v] || aid[v] > 0) && !P.valid(&P, next + v * ps)) bad = v + 1;
+    counters[0] = gathered; counters[1] = processed; counters[2] = changed; counters[3] = bad;
+    return OG_OK;
+}
+
 /* ---------------------------------------------------------------------------
  * metrics.cpp
  * ------------------------------------------------------------------------- */

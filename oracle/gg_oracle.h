@@ -109,6 +109,19 @@ int og_run(const og_graph* g, int prog, const og_params* params,
            uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
            char* msg, size_t msg_cap);
 
+/* One iteration of engine.hpp:194-224 restricted to destinations
+ * [v_begin, v_end) — the per-rank step of a destination partition (used by
+ * the multi-rank protocol tests). prev/next/status/status_next/aid are
+ * global-length arrays; only the owned range of next/status_next/aid/flags
+ * is written. counters: [gathered, processed, changed, bad_vertex+1 (0 =
+ * none; the smallest invalid owned vertex checked like :228-230)]. */
+int og_step_range(const og_graph* g, int prog, const og_params* params, int mode, double theta,
+                  uint8_t* flags, uint32_t* aid, const void* prev, const uint8_t* status,
+                  void* next, uint8_t* status_next, uint64_t v_begin, uint64_t v_end,
+                  uint64_t counters[4]);
+/* Initial property of every vertex (engine.hpp:163-164) into out. */
+int og_init_props(const og_graph* g, int prog, const og_params* params, void* out);
+
 /* metrics.cpp */
 int og_topk_error(const double* approx, const double* exact, uint64_t n,
                   uint64_t k, double* err);

@@ -168,6 +168,10 @@ class Oracle:
                                  C.c_char_p, C.c_size_t]
             L.og_mix64.argtypes = [C.c_uint64]
             L.og_mix64.restype = C.c_uint64
+            L.og_init_props.argtypes = [G, C.c_int, C.POINTER(_Params), C.c_void_p]
+            L.og_step_range.argtypes = [G, C.c_int, C.POINTER(_Params), C.c_int, C.c_double,
+                                        u8p, u32p, C.c_void_p, u8p, C.c_void_p, u8p, C.c_uint64,
+                                        C.c_uint64, u64p]
             for m in ("og_relative_error", "og_stretch_error"):
                 getattr(L, m).argtypes = [f64p, f64p, C.c_uint64, C.POINTER(C.c_double)]
             L.og_topk_error.argtypes = [f64p, f64p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]
@@ -298,6 +302,35 @@ class Oracle:
                       int(summ.iterations_run), int(summ.total_processed_edges),
                       int(summ.err_iteration), int(summ.err_vertex), msg.value.decode(),
                       flags[:g.e] if flags is not None else None)
+
+    # -- per-range step (multi-rank protocol tests) ----------------------------
+    class Stepper:
+        """Holds an oracle graph and runs og_step_range on numpy state."""
+
+        def __init__(self, g: CSC, prog, **pp):
+            self.g, self.prog = g, prog
+            self.params = _params(prog, **pp)
+            self.gp = Oracle._ptr(g)
+            self.states = pp.get("states", 2)
+
+        def init_props(self):
+            props = _prop_shape(self.prog, self.g.n, self.states)
+            Oracle.lib().og_init_props(self.gp, self.prog, C.byref(self.params), props.ctypes.data)
+            return props
+
+        def step(self, mode, theta, flags, aid, prev, status, nxt, status_next, vb, ve):
+            ctr = np.zeros(4, np.uint64)
+            rc = Oracle.lib().og_step_range(self.gp, self.prog, C.byref(self.params), mode, theta,
+                                            flags, aid, prev.ctypes.data, status, nxt.ctypes.data,
+                                            status_next, vb, ve, ctr)
+            if rc:
+                raise ValueError("og_step_range failed")
+            return ctr
+
+        def close(self):
+            if self.gp:
+                Oracle.lib().og_free_graph(self.gp)
+                self.gp = None
 
     # -- metrics ------------------------------------------------------------
     @classmethod

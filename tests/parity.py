@@ -17,6 +17,41 @@ from oracle.oracle import BP, BP_EDGE, PR, SCHEMES, SSSP, WCC, Oracle
 RTOL = {PR: 1e-9, BP: 1e-6, BP_EDGE: 2e-6}
 
 
+class _OracleReport:
+    def __init__(self, r):
+        self.final_properties = r.props
+        self.iterations_run = r.iterations_run
+        self.total_processed_edges = r.total_processed_edges
+        self.total_wall_seconds = 0.0
+        self.per_iteration = r.processed_edges
+
+
+def oracle_runner(graph, program, cfg):
+    """runner(graph, program, EngineConfig) for paper_2104_10039_b200.sweep
+    backed by the CPU oracle (tests only)."""
+    import paper_2104_10039_b200 as ggb
+    from oracle.oracle import CSC
+    g = CSC(graph.n, graph.in_offsets, graph.in_sources,
+            None if graph.weights is None else graph.weights.astype(np.float64), graph.out_degree)
+    c = cfg.c()
+    kw = dict(scheme=c.scheme, sigma=c.sigma, theta=c.theta, alpha=c.alpha,
+              max_iterations=c.max_iterations, seed=c.seed, threads=max(c.threads, 1))
+    if isinstance(program, ggb.PageRankProgram):
+        r = Oracle.run(g, PR, damping=program.damping, epsilon=program.epsilon, **kw)
+    elif isinstance(program, ggb.SsspProgram):
+        r = Oracle.run(g, SSSP, source=program.source, graded=program.graded, **kw)
+    elif isinstance(program, ggb.WccProgram):
+        r = Oracle.run(g, WCC, **kw)
+    elif isinstance(program, ggb.BeliefPropagationProgram):
+        r = Oracle.run(g, BP, states=program.states, coupling=program.coupling,
+                       epsilon=program.epsilon, **kw)
+    else:
+        raise TypeError(type(program))
+    if r.status != 0:
+        raise RuntimeError(r.msg)
+    return _OracleReport(r)
+
+
 def to_graph(ggb, g, weights=None):
     w = g.w if weights is None else weights
     return ggb.Graph(g.n, g.off, g.src, w, g.outdeg)
