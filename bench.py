@@ -220,30 +220,34 @@ def ours(args):
     full = [it for it in per if it.mode != ggb.IterationMode.approximate]
     frac_rank = info["e_local"] / max(e, 1)
 
-    def gteps(its):
+    def gteps(its):  # gather step (edge + vertex kernels) of this rank
         t = sum(i.kernel_ms for i in its)
         return (sum(i.processed_edges for i in its) * frac_rank / (t / 1e3) / 1e9) if t else None
 
-    def gbs(its):
-        t = sum(i.kernel_ms for i in its)
-        return (sum(i.algo_bytes for i in its) * frac_rank / (t / 1e3) / 1e9) if t else None
+    def gbs(its, b="edge_bytes", m="edge_ms"):  # algorithmic bytes / CUDA-event time
+        t = sum(getattr(i, m) for i in its)
+        return (sum(getattr(i, b) for i in its) / (t / 1e3) / 1e9) if t else None
 
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs", 6650.0)
-    dom = approx if approx else full
+    dom = approx if approx else full  # the dominant kernel: the approximate edge gather
     achieved = gbs(dom)
     traffic, ncu = load_traffic(args.workload)
     roofline = {
-        "bound": "hbm", "kernel": "iteration_kernel (approximate gather, sparsified CSC)"
-        if approx else "iteration_kernel (full gather)",
+        "bound": "hbm", "kernel": "edge_kernel<kEdgePlain> (approximate gather, sparsified CSC)"
+        if approx else "edge_kernel (full gather)",
         "achieved": round(achieved, 1) if achieved else None, "peak": peak,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if "hbm_gbs" in peaks
         else "fallback 6650 GB/s (B200_PROFILING.md)",
         "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
-        "algo_bytes_per_launch": int(sum(i.algo_bytes for i in dom) / max(len(dom), 1) * frac_rank),
-        "kernel_ms_per_launch": sum(i.kernel_ms for i in dom) / max(len(dom), 1),
-        "full_gather_achieved_gbs": round(gbs(full), 1) if gbs(full) else None,
+        "algo_bytes_per_launch": int(sum(i.edge_bytes for i in dom) / max(len(dom), 1)),
+        "bytes_model": "E_p * (4 src + sizeof(message) + sizeof(weight)); SURVEY §8(d) b_e",
+        "kernel_ms_per_launch": round(sum(i.edge_ms for i in dom) / max(len(dom), 1), 4),
+        "launches": len(dom),
+        "vertex_kernel_gbs": round(gbs(per, "vertex_bytes", "vertex_ms"), 1)
+        if gbs(per, "vertex_bytes", "vertex_ms") else None,
+        "full_gather_edge_gbs": round(gbs(full), 1) if gbs(full) else None,
     }
 
     # ---- end to end through the public API: pinned host CSC -> H2D upload
@@ -265,10 +269,14 @@ def ours(args):
         h2d = (info["v_end"] - info["v_begin"] + 1) * 8 + info["e_local"] * (4 + wsz) + n * 4
         d2h = n * prop_bytes(wl)
 
+        out_shape = {"pr": (n,), "sssp": (n,), "wcc": (n,), "bp": (n, 2)}[wl["prog"]]
+        out_dt = np.uint32 if wl["prog"] == "wcc" else np.float64
+        out_buf = pinned(int(np.prod(out_shape)), out_dt).reshape(out_shape)
+
         def e2e_step():
             g2 = ggb.DeviceGraph.upload(host, device=local, rank=rank, nranks=world,
                                         exchange=exchange.handle if exchange else None)
-            r = ggb.run(g2, program, cfg)
+            r = ggb.run(g2, program, cfg, out=out_buf)
             g2.close()
             return r
         for _ in range(args.warmup):

@@ -273,16 +273,16 @@ __global__ void relabel_kernel(uint32_t* __restrict__ src, uint64_t count,
 
 void assign_slots(DevGraph& g) {
     const uint64_t n = g.n;
-    GGB_CUDA(cudaMalloc(&g.slot_of, (n + 1) * 4));
-    GGB_CUDA(cudaMalloc(&g.vtx_of_slot, (n + 1) * 4));
+    g.slot_of = static_cast<decltype(g.slot_of)>(dev_alloc((n + 1) * 4, g.stream));
+    g.vtx_of_slot = static_cast<decltype(g.vtx_of_slot)>(dev_alloc((n + 1) * 4, g.stream));
     if (n == 0) return;
     uint64_t *k0 = nullptr, *k1 = nullptr, *db = nullptr;
     uint32_t *v0 = nullptr, *v1 = nullptr;
-    GGB_CUDA(cudaMalloc(&k0, n * 8));
-    GGB_CUDA(cudaMalloc(&k1, n * 8));
-    GGB_CUDA(cudaMalloc(&v0, n * 4));
-    GGB_CUDA(cudaMalloc(&v1, n * 4));
-    GGB_CUDA(cudaMalloc(&db, g.bounds.size() * 8));
+    k0 = static_cast<decltype(k0)>(dev_alloc(n * 8, g.stream));
+    k1 = static_cast<decltype(k1)>(dev_alloc(n * 8, g.stream));
+    v0 = static_cast<decltype(v0)>(dev_alloc(n * 4, g.stream));
+    v1 = static_cast<decltype(v1)>(dev_alloc(n * 4, g.stream));
+    db = static_cast<decltype(db)>(dev_alloc(g.bounds.size() * 8, g.stream));
     GGB_CUDA(cudaMemcpyAsync(db, g.bounds.data(), g.bounds.size() * 8, cudaMemcpyHostToDevice,
                              g.stream));
     slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, k0, v0);
@@ -293,7 +293,7 @@ void assign_slots(DevGraph& g) {
     GGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
                                              g.stream));
     void* tmpp = nullptr;
-    GGB_CUDA(cudaMalloc(&tmpp, tmp));
+    tmpp = static_cast<decltype(tmpp)>(dev_alloc(tmp, g.stream));
     GGB_CUDA(cub::DeviceRadixSort::SortPairs(tmpp, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
                                              g.stream));
     slot_fill_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(v1, n, g.slot_of, g.vtx_of_slot);
@@ -304,7 +304,7 @@ void assign_slots(DevGraph& g) {
         GGB_CUDA(cudaGetLastError());
     }
     GGB_CUDA(cudaStreamSynchronize(g.stream));
-    cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1); cudaFree(db); cudaFree(tmpp);
+    dev_free(k0, g.stream); dev_free(k1, g.stream); dev_free(v0, g.stream); dev_free(v1, g.stream); dev_free(db, g.stream); dev_free(tmpp, g.stream);
 }
 
 __global__ void unlabel_kernel(const uint32_t* __restrict__ src, uint64_t count,
@@ -316,13 +316,13 @@ __global__ void unlabel_kernel(const uint32_t* __restrict__ src, uint64_t count,
 
 void export_sources(const DevGraph& g, uint32_t* host_out) {
     uint32_t* tmp = nullptr;
-    GGB_CUDA(cudaMalloc(&tmp, (g.e_loc + 1) * 4));
+    tmp = static_cast<decltype(tmp)>(dev_alloc((g.e_loc + 1) * 4, g.stream));
     unlabel_kernel<<<grid_for(g.e_loc, 256), 256, 0, g.stream>>>(g.src + g.full.pad, g.e_loc,
                                                                   g.vtx_of_slot, tmp);
     GGB_CUDA(cudaGetLastError());
     GGB_CUDA(cudaMemcpyAsync(host_out, tmp, g.e_loc * 4, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
-    cudaFree(tmp);
+    dev_free(tmp, g.stream);
 }
 
 __global__ void superstep_invalid_kernel(uint32_t nloc, uint32_t v_begin,
@@ -349,13 +349,16 @@ DevGraph::~DevGraph() {
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
-    if (off) cudaFree(off);
-    if (src) cudaFree(src);
-    if (w) cudaFree(w);
-    if (outdeg) cudaFree(outdeg);
-    if (slot_of) cudaFree(slot_of);
-    if (vtx_of_slot) cudaFree(vtx_of_slot);
-    if (stream) cudaStreamDestroy(stream);
+    dev_free(off, stream);
+    dev_free(src, stream);
+    dev_free(w, stream);
+    dev_free(outdeg, stream);
+    dev_free(slot_of, stream);
+    dev_free(vtx_of_slot, stream);
+    if (stream) {
+        cudaStreamSynchronize(stream);
+        cudaStreamDestroy(stream);
+    }
 }
 
 }  // namespace ggb

@@ -49,6 +49,13 @@ static void setup_common(DevGraph& g, const gg_part_opts* opts) {
         throw Error(GG_CUDA, std::string("libggb.so needs an sm_100 device, found ") + prop.name);
     g.num_sms = prop.multiProcessorCount;
     GGB_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    g.ws.stream = g.stream;
+    // keep freed device memory cached in the stream-ordered pool (graphs are
+    // re-created on the end-to-end path; see graph.cuh dev_alloc)
+    cudaMemPool_t pool;
+    GGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t threshold = UINT64_MAX;
+    GGB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     g.rank = opts ? opts->rank : 0;
     g.nranks = opts ? std::max(1, opts->nranks) : 1;
     g.exchange = opts ? static_cast<gg_exchange*>(opts->exchange) : nullptr;
@@ -57,8 +64,8 @@ static void setup_common(DevGraph& g, const gg_part_opts* opts) {
     if (g.rank < 0 || g.rank >= g.nranks) throw Error(GG_INVALID_ARGUMENT, "rank out of range");
 }
 
-static void finish_graph(DevGraph& g, const std::vector<uint64_t>& host_off_full) {
-    g.bounds = plan_partition(g.n, host_off_full.data(), g.nranks);
+static void finish_graph(DevGraph& g, const uint64_t* host_off_full) {
+    g.bounds = plan_partition(g.n, host_off_full, g.nranks);
     g.ebounds.resize(g.nranks + 1);
     for (int r = 0; r <= g.nranks; ++r) g.ebounds[r] = host_off_full[g.bounds[r]];
     g.v_begin = g.bounds[g.rank];
@@ -115,24 +122,25 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
             g.n = csc->n;
             g.e_global = csc->e;
             g.wkind = csc->weight_kind;
-            std::vector<uint64_t> off(csc->offsets ? csc->offsets : nullptr,
-                                      csc->offsets ? csc->offsets + csc->n + 1 : nullptr);
-            if (off.empty()) off.assign(1, 0);
-            finish_graph(g, off);
+            const uint64_t zero = 0;
+            finish_graph(g, csc->offsets ? csc->offsets : &zero);
             const uint64_t pad = g.e_base % kChunkEdges;  // padded = global position mod 512
-            GGB_CUDA(cudaMalloc(&g.off, (g.nloc + 1) * 8));
-            GGB_CUDA(cudaMalloc(&g.src, (pad + g.e_loc + kRun) * 4));
-            GGB_CUDA(cudaMalloc(&g.outdeg, (g.n + 1) * 4));
-            std::vector<uint64_t> loc(g.nloc + 1);
-            for (uint64_t i = 0; i <= g.nloc; ++i) loc[i] = off[g.v_begin + i] - g.e_base;
-            GGB_CUDA(cudaMemcpyAsync(g.off, loc.data(), (g.nloc + 1) * 8, cudaMemcpyHostToDevice,
-                                     g.stream));
+            g.off = static_cast<decltype(g.off)>(dev_alloc((g.nloc + 1) * 8, g.stream));
+            g.src = static_cast<decltype(g.src)>(dev_alloc((pad + g.e_loc + kRun) * 4, g.stream));
+            g.outdeg = static_cast<decltype(g.outdeg)>(dev_alloc((g.n + 1) * 4, g.stream));
+            // the owned offsets straight from the caller's buffer, rebased on device
+            GGB_CUDA(cudaMemcpyAsync(g.off, csc->offsets ? csc->offsets + g.v_begin : &zero,
+                                     (g.nloc + 1) * 8, cudaMemcpyHostToDevice, g.stream));
+            if (g.e_base) {
+                rebase_kernel<<<256, 256, 0, g.stream>>>(g.off, g.nloc + 1, g.e_base, g.off);
+                GGB_CUDA(cudaGetLastError());
+            }
             if (g.e_loc)
                 GGB_CUDA(cudaMemcpyAsync(g.src + pad, csc->sources + g.e_base, g.e_loc * 4,
                                          cudaMemcpyHostToDevice, g.stream));
             const size_t wb = weight_size(g.wkind);
             if (wb) {
-                GGB_CUDA(cudaMalloc(&g.w, (pad + g.e_loc + kRun) * wb));
+                g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
                 if (g.e_loc)
                     GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
                                              static_cast<const char*>(csc->weights) + g.e_base * wb,
@@ -179,34 +187,36 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
             g.e_global = r.e;
             g.wkind = p->weight_kind;
             std::vector<uint64_t> off(r.n + 1);
-            GGB_CUDA(cudaMemcpy(off.data(), r.off, (r.n + 1) * 8, cudaMemcpyDeviceToHost));
-            finish_graph(g, off);
+            GGB_CUDA(cudaMemcpyAsync(off.data(), r.off, (r.n + 1) * 8, cudaMemcpyDeviceToHost,
+                                     g.stream));
+            GGB_CUDA(cudaStreamSynchronize(g.stream));
+            finish_graph(g, off.data());
             g.outdeg = r.outdeg;
             if (g.nranks == 1) {
                 g.off = r.off;
                 g.src = r.src;
                 g.w = r.w;
             } else {
-                GGB_CUDA(cudaMalloc(&g.off, (g.nloc + 1) * 8));
+                g.off = static_cast<decltype(g.off)>(dev_alloc((g.nloc + 1) * 8, g.stream));
                 rebase_kernel<<<256, 256, 0, g.stream>>>(r.off + g.v_begin, g.nloc + 1, g.e_base,
                                                           g.off);
                 GGB_CUDA(cudaGetLastError());
                 const uint64_t pad = g.e_base % kChunkEdges;
-                GGB_CUDA(cudaMalloc(&g.src, (pad + g.e_loc + kRun) * 4));
+                g.src = static_cast<decltype(g.src)>(dev_alloc((pad + g.e_loc + kRun) * 4, g.stream));
                 GGB_CUDA(cudaMemcpyAsync(g.src + pad, r.src + g.e_base, g.e_loc * 4,
                                          cudaMemcpyDeviceToDevice, g.stream));
                 const size_t wb = weight_size(g.wkind);
                 if (wb) {
-                    GGB_CUDA(cudaMalloc(&g.w, (pad + g.e_loc + kRun) * wb));
+                    g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
                     GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
                                              static_cast<char*>(r.w) + g.e_base * wb,
                                              g.e_loc * wb, cudaMemcpyDeviceToDevice, g.stream));
                 }
                 g.full.pad = pad;
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
-                cudaFree(r.off);
-                cudaFree(r.src);
-                if (r.w) cudaFree(r.w);
+                dev_free(r.off, g.stream);
+                dev_free(r.src, g.stream);
+                if (r.w) dev_free(r.w, g.stream);
             }
             assign_slots(g);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
@@ -264,10 +274,10 @@ gg_status gg_dev_graph_export(const gg_dev_graph* h, uint64_t* offsets, uint32_t
 gg_status gg_bp_priors(uint64_t n, uint64_t seed, float* out) {
     return guarded(nullptr, [&] {
         float* d = nullptr;
-        GGB_CUDA(cudaMalloc(&d, (2 * n + 2) * 4));
+        d = static_cast<decltype(d)>(dev_alloc((2 * n + 2) * 4, 0));
         bp_priors_device(n, seed, d, 0);
         GGB_CUDA(cudaMemcpy(out, d, 2 * n * 4, cudaMemcpyDeviceToHost));
-        GGB_CUDA(cudaFree(d));
+        dev_free(d, 0);
     });
 }
 

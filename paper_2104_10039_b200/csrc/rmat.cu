@@ -112,18 +112,18 @@ RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st) {
     out.n = n;
     if (m >= (1ull << 31)) throw Error(GG_INVALID_ARGUMENT, "rmat: at most 2^31-1 raw edges");
     uint64_t *k0 = nullptr, *k1 = nullptr;
-    GGB_CUDA(cudaMalloc(&k0, (m + 1) * 8));
-    GGB_CUDA(cudaMalloc(&k1, (m + 1) * 8));
+    k0 = static_cast<decltype(k0)>(dev_alloc((m + 1) * 8, st));
+    k1 = static_cast<decltype(k1)>(dev_alloc((m + 1) * 8, st));
     rmat_keys_kernel<<<g1(m), 256, 0, st>>>(m, p.scale, mix64(p.seed), p.a, p.a + p.b,
                                             p.a + p.b + p.c, k0);
     GGB_CUDA(cudaGetLastError());
     size_t tmp_sort = 0, tmp_uniq = 0;
     int* d_num = nullptr;
-    GGB_CUDA(cudaMalloc(&d_num, 8));
+    d_num = static_cast<decltype(d_num)>(dev_alloc(8, st));
     GGB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_sort, k0, k1, m, 0, 2 * p.scale + 1, st));
     GGB_CUDA(cub::DeviceSelect::Unique(nullptr, tmp_uniq, k1, k0, d_num, m, st));
     void* tmp = nullptr;
-    GGB_CUDA(cudaMalloc(&tmp, std::max(tmp_sort, tmp_uniq)));
+    tmp = static_cast<decltype(tmp)>(dev_alloc(std::max(tmp_sort, tmp_uniq), st));
     GGB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_sort, k0, k1, m, 0, 2 * p.scale + 1, st));
     GGB_CUDA(cub::DeviceSelect::Unique(tmp, tmp_uniq, k1, k0, d_num, m, st));
     int num = 0;
@@ -138,54 +138,54 @@ RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st) {
     uint64_t* keys = k0;
     uint32_t dshift = p.scale;
     if (p.symmetrize) {
-        GGB_CUDA(cudaFree(k1));
+        dev_free(k1, st);
         k1 = nullptr;
         uint64_t *s0 = nullptr, *s1 = nullptr;
-        GGB_CUDA(cudaMalloc(&s0, (2 * e + 1) * 8));
+        s0 = static_cast<decltype(s0)>(dev_alloc((2 * e + 1) * 8, st));
         sym_keys_kernel<<<g1(e), 256, 0, st>>>(k0, e, p.scale, s0);
         GGB_CUDA(cudaGetLastError());
         GGB_CUDA(cudaStreamSynchronize(st));
-        GGB_CUDA(cudaFree(k0));
+        dev_free(k0, st);
         k0 = nullptr;
-        GGB_CUDA(cudaMalloc(&s1, (2 * e + 1) * 8));
+        s1 = static_cast<decltype(s1)>(dev_alloc((2 * e + 1) * 8, st));
         size_t t2 = 0;
         GGB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t2, s0, s1, 2 * e, 0, 2 * p.scale + 2, st));
         if (t2 > std::max(tmp_sort, tmp_uniq)) {
-            GGB_CUDA(cudaFree(tmp));
-            GGB_CUDA(cudaMalloc(&tmp, t2));
+            dev_free(tmp, st);
+            tmp = static_cast<decltype(tmp)>(dev_alloc(t2, st));
         }
         GGB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, t2, s0, s1, 2 * e, 0, 2 * p.scale + 2, st));
         GGB_CUDA(cudaStreamSynchronize(st));
-        GGB_CUDA(cudaFree(s0));
+        dev_free(s0, st);
         keys = s1;
         k0 = s1;
         e = 2 * e;
         dshift = p.scale + 1;
     }
     out.e = e;
-    GGB_CUDA(cudaMalloc(&out.off, (n + 1) * 8));
-    GGB_CUDA(cudaMalloc(&out.src, (e + 1) * 4));
-    GGB_CUDA(cudaMalloc(&out.outdeg, n * 4));
+    out.off = static_cast<decltype(out.off)>(dev_alloc((n + 1) * 8, st));
+    out.src = static_cast<decltype(out.src)>(dev_alloc((e + 1) * 4, st));
+    out.outdeg = static_cast<decltype(out.outdeg)>(dev_alloc(n * 4, st));
     GGB_CUDA(cudaMemsetAsync(out.outdeg, 0, n * 4, st));
     csc_from_keys_kernel<<<g1(e + 1), 256, 0, st>>>(keys, e, n, p.scale, dshift, out.src, out.off);
     GGB_CUDA(cudaGetLastError());
     outdeg_kernel<<<g1(e), 256, 0, st>>>(out.src, e, out.outdeg);
     GGB_CUDA(cudaGetLastError());
     if (p.weight_kind == GG_W_U32) {
-        GGB_CUDA(cudaMalloc(&out.w, (e + 1) * 4));
+        out.w = static_cast<decltype(out.w)>(dev_alloc((e + 1) * 4, st));
         weights_u32_kernel<<<g1(e), 256, 0, st>>>(e, p.seed, static_cast<uint32_t*>(out.w));
     } else if (p.weight_kind == GG_W_F32) {
-        GGB_CUDA(cudaMalloc(&out.w, (e + 1) * 4));
+        out.w = static_cast<decltype(out.w)>(dev_alloc((e + 1) * 4, st));
         couplings_kernel<<<g1(e), 256, 0, st>>>(e, p.seed, static_cast<float*>(out.w));
     } else if (p.weight_kind != GG_W_NONE) {
         throw Error(GG_INVALID_ARGUMENT, "rmat weight_kind must be none, u32 or f32");
     }
     GGB_CUDA(cudaGetLastError());
     GGB_CUDA(cudaStreamSynchronize(st));
-    if (k0) cudaFree(k0);
-    if (k1) cudaFree(k1);
-    cudaFree(tmp);
-    cudaFree(d_num);
+    if (k0) dev_free(k0, st);
+    if (k1) dev_free(k1, st);
+    dev_free(tmp, st);
+    dev_free(d_num, st);
     return out;
 }
 

@@ -328,13 +328,24 @@ def unpack_bitmap(words: np.ndarray, e: int) -> np.ndarray:
     return np.unpackbits(words.view(np.uint8), bitorder="little")[:e].astype(np.uint8)
 
 
+def _out_buffer(out, shape, dtype):
+    if out is None:
+        return np.zeros(shape, dtype)
+    if out.dtype != np.dtype(dtype) or out.shape != (shape if isinstance(shape, tuple) else (shape,)) \
+            or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"out must be a C-contiguous {np.dtype(dtype).name} array of shape {shape}")
+    return out
+
+
 def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: bool = False,
-        rec_cap: int | None = None, device_output: bool = False) -> RunReport:
+        rec_cap: int | None = None, device_output: bool = False, out=None) -> RunReport:
     """gg::run (engine.hpp:141-249) on the device. `graph` is a Graph
     (uploaded for the call) or a DeviceGraph (already resident).
     timing: CUDA-event time of every kernel into the records.
     device_output: leave the final properties in HBM (no D2H copy;
-    final_properties is then None)."""
+    final_properties is then None).
+    out: caller-owned result array (e.g. pinned host memory) of the
+    program's property shape/dtype, filled instead of a fresh array."""
     ccfg = cfg.c()
     owned = None
     if isinstance(graph, Graph):
@@ -353,21 +364,21 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         err = L.ErrorC()
         lib = L.lib()
         if isinstance(program, PageRankProgram):
-            props = np.zeros(n, np.float64)
+            props = _out_buffer(out, n, np.float64)
             p = L.PrParams(program.damping, program.epsilon)
             rc = lib.gg_run_pr(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                C.byref(summ), C.byref(opts), C.byref(err))
         elif isinstance(program, SsspProgram):
-            props = np.zeros(n, np.float64)
+            props = _out_buffer(out, n, np.float64)
             p = L.SsspParams(program.source, int(program.graded))
             rc = lib.gg_run_sssp(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                  C.byref(summ), C.byref(opts), C.byref(err))
         elif isinstance(program, WccProgram):
-            props = np.zeros(n, np.uint32)
+            props = _out_buffer(out, n, np.uint32)
             rc = lib.gg_run_wcc(dg._h, C.byref(ccfg), props.ctypes.data, recs, cap,
                                 C.byref(summ), C.byref(opts), C.byref(err))
         elif isinstance(program, BeliefPropagationProgram):
-            props = np.zeros((n, program.states), np.float64)
+            props = _out_buffer(out, (n, program.states), np.float64)
             p = L.BpParams(program.states, program.coupling, program.epsilon, None)
             rc = lib.gg_run_bp(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                C.byref(summ), C.byref(opts), C.byref(err))
@@ -375,7 +386,7 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
             pri = np.ascontiguousarray(program.priors, np.float32).reshape(-1)
             if pri.shape[0] != 2 * n:
                 raise ValueError("edge BP needs a float32[n, 2] prior table")
-            props = np.zeros((n, 2), np.float64)
+            props = _out_buffer(out, (n, 2), np.float64)
             p = L.BpParams(2, 0.0, program.epsilon, pri.ctypes.data)
             rc = lib.gg_run_bp(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                C.byref(summ), C.byref(opts), C.byref(err))
