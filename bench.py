@@ -241,6 +241,9 @@ def ours(args):
         else "fallback 6650 GB/s (B200_PROFILING.md)",
         "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
         "traffic": traffic,
+        "traffic_source": (f"profiles/ncu_{args.workload}.json: ncu --set full, dram read+write of one "
+                           f"launch with {ncu['dominant_kernel_algo_bytes_per_launch']} algorithmic bytes"
+                           if ncu else None),
         "algo_bytes_per_launch": int(sum(i.edge_bytes for i in dom) / max(len(dom), 1)),
         "bytes_model": "E_p * (4 src + sizeof(message) + sizeof(weight)); SURVEY §8(d) b_e",
         "kernel_ms_per_launch": round(sum(i.edge_ms for i in dom) / max(len(dom), 1), 4),
