@@ -1,20 +1,18 @@
 // graph.cuh — HBM-resident pull CSC (gg::Graph, graph.hpp:29-49) and the
 // per-graph device workspace.
 //
-// HBM layout per rank (local = owned destination range [v_begin, v_end)):
-//   off      u64[nloc+1]   local in-edge offsets (rebased to 0)
-//   src      u32[e_loc]    in-edge sources, GLOBAL vertex ids
-//   w        W[e_loc]      none | u32 | f32 | f64
-//   outdeg   u32[n]        out-degree of every (global) vertex
-//   tasks    uint4[]       {window, chunk, nchunks, slot} work list of the full CSC
-//   mtasks   uint4[]       the chunks of multi-chunk windows
-// Run workspace (allocated once, reused across runs):
-//   bitmap   u32[e_loc/32+1] active-edge flags (EdgeFlags, graph.hpp:54-72,
-//                            one BIT per edge instead of one byte)
-//   wprefix  u64[words+1]    exclusive popcount prefix of the bitmap
-//   s_off/s_src/s_w          sparsified CSC (only flagged edges, same order)
-//   s_tasks/s_mtasks         its work lists
-//   msg[2], prop, status[2], partials, tickets, counters
+// HBM layout per rank (local = owned destination range [v_begin, v_end)),
+// see DESIGN.md §3:
+//   off      u64[nloc+1]        local in-edge offsets (rebased to 0)
+//   src      u32[pad+e_loc+..]  in-edge sources as MESSAGE SLOT ids, at padded
+//                               positions pad + local edge (pad = global pos mod 512)
+//   w        W[...]             none | u32 | f32 | f64, padded likewise
+//   outdeg   u32[n]             out-degree of every (global) vertex
+//   slot_of / vtx_of_slot       hot-first message slot map (global)
+//   full     ListMeta           run -> non-empty-vertex map of the full list
+// Run workspace (Workspace, grow-only, reused across runs): bitmap (1 bit per
+// local edge, EdgeFlags graph.hpp:54-72), sparsified s_off/s_src/s_w + its
+// ListMeta, msg[2], prop, status[2], acc_out/hv/tv/carry, counters.
 #pragma once
 
 #include <map>
