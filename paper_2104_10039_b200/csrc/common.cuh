@@ -114,36 +114,36 @@ __device__ __forceinline__ T shfl_idx_any(T v, int lane) {
 // per-vertex message array is re-read randomly (evict_last).
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 // Streaming (read-once) 32-bit load: bypass L1, evict-first in L2.
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
                  : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 // Random message loads, kept in L2.
 __device__ __forceinline__ uint32_t ld_keep(const uint32_t* p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ uint2 ld_keep(const uint2* p, uint64_t pol) {
     uint2 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
                  : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ uint4 ld_keep(const uint4* p, uint64_t pol) {
     uint4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
@@ -206,7 +206,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 

@@ -139,13 +139,14 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
             s[j] = (p >= lo && p < hi) ? ld_stream_u32(a.src + p, pol_stream) : 0u;
         }
     }
+    // Every gather is issued unconditionally and independently (positions
+    // outside [lo, hi) read slot 0, always L2-resident; their values are never
+    // folded), so all 16 are in flight together. The weights of a run lie
+    // inside the padded allocation.
 #pragma unroll
     for (int j = 0; j < kRun; ++j) {
-        const uint64_t p = P0 + j;
-        if (p >= lo && p < hi) {
-            m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
-            if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + p);
-        }
+        m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
+        if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + P0 + j);
     }
 }
 
