@@ -11,6 +11,9 @@
 #include <cub/cub.cuh>
 
 #include "exchange.cuh"
+#include <cmath>
+#include <type_traits>
+
 #include "graph.cuh"
 #include "kernels.cuh"
 
@@ -43,23 +46,21 @@ static inline unsigned grid_for(uint64_t n, int block, uint64_t cap = 148ull * 6
 // sparsify (engine.cpp:63-75): u = (mix64(mix64(seed) ^ e) >> 11) * 2^-53,
 // flag = u < sigma, hashed on the GLOBAL edge id so every partition agrees.
 // --------------------------------------------------------------------------
+// engine.cpp:63-75: flag(e) = (mix64(key ^ e) >> 11) * 2^-53 < sigma.
+// The product is exact (a 53-bit integer times a power of two), so the test
+// is the integer compare (mix64(key ^ e) >> 11) < ceil(sigma * 2^53) = thr.
+// One thread per bitmap word (32 independent hashes in flight).
 __global__ void sparsify_kernel(uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_loc,
-                                uint64_t e_base, double sigma, uint64_t key, int all_ones) {
+                                uint64_t e_base, uint64_t thr, uint64_t key) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nwords;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t word = 0;
         if (i < nwords) {
-#pragma unroll 4
+            const uint64_t e0 = i * 32;
+            const int nb = e_loc - e0 < 32 ? (int)(e_loc - e0) : 32;
+#pragma unroll 8
             for (int b = 0; b < 32; ++b) {
-                const uint64_t e = i * 32 + b;
-                if (e >= e_loc) break;
-                bool f;
-                if (all_ones) {
-                    f = true;
-                } else {
-                    const double u = (double)(mix64(key ^ (e_base + e)) >> 11) * 0x1.0p-53;
-                    f = u < sigma;
-                }
+                const bool f = b < nb && (mix64(key ^ (e_base + e0 + b)) >> 11) < thr;
                 word |= (f ? 1u : 0u) << b;
             }
         }
@@ -69,8 +70,9 @@ __global__ void sparsify_kernel(uint32_t* __restrict__ bitmap, uint64_t nwords, 
 
 void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
+    const uint64_t thr = all_ones ? (1ull << 53) : (uint64_t)std::ceil(sigma * 0x1.0p53);
     sparsify_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(
-        bitmap, nwords, g.e_loc, g.e_base, sigma, mix64(seed), all_ones ? 1 : 0);
+        bitmap, nwords, g.e_loc, g.e_base, thr, mix64(seed));
     GGB_CUDA(cudaGetLastError());
 }
 
@@ -170,26 +172,43 @@ __global__ void soff_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
         s_off[v] = bit_rank(bitmap, wpref, off[v]);
 }
 
+// Stream compaction of the kept edges (sources, weights) into the padded
+// sparsified list. A warp takes 8 bitmap words (256 edges) per step: lane l
+// owns bit l of each word; all loads of the step are issued before any store,
+// so one memory latency covers 256 edges.
 template <int WB>
 __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w,
                                uint64_t e_loc, uint64_t in_pad, const uint32_t* __restrict__ bitmap,
                                const uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
                                void* __restrict__ s_w, uint64_t out_pad) {
-    // warp-aligned: lane == e & 31, so the word and its prefix are shared
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < e_loc;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t word = __ldg(bitmap + (e >> 5));
-        const uint32_t b = (uint32_t)(e & 31);
-        if ((word >> b) & 1u) {
-            const uint64_t pos = out_pad + __ldg(wpref + (e >> 5)) +
-                                 (uint64_t)__popc(word & ((1u << b) - 1u));
-            s_src[pos] = __ldg(src + in_pad + e);
-            if constexpr (WB == 4)
-                static_cast<uint32_t*>(s_w)[pos] =
-                    __ldg(static_cast<const uint32_t*>(w) + in_pad + e);
-            if constexpr (WB == 8)
-                static_cast<unsigned long long*>(s_w)[pos] =
-                    __ldg(static_cast<const unsigned long long*>(w) + in_pad + e);
+    using WT = std::conditional_t<WB == 8, unsigned long long, uint32_t>;
+    constexpr int kW = 8;
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t nw = (e_loc + 31) / 32;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t w0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * kW; w0 < nw;
+         w0 += warps * kW) {
+        uint32_t word[kW], sv[kW];
+        uint64_t base[kW];
+        WT wv[kW];
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            const bool in = w0 + k < nw;
+            word[k] = in ? __ldg(bitmap + w0 + k) : 0u;
+            base[k] = in ? __ldg(wpref + w0 + k) : 0ull;
+            const uint64_t e = (w0 + k) * 32 + lane;
+            const bool ine = e < e_loc;
+            sv[k] = ine ? __ldg(src + in_pad + e) : 0u;
+            if constexpr (WB != 0) wv[k] = ine ? __ldg(static_cast<const WT*>(w) + in_pad + e) : WT(0);
+        }
+#pragma unroll
+        for (int k = 0; k < kW; ++k) {
+            if ((word[k] >> lane) & 1u) {
+                const uint64_t pos = out_pad + base[k] + (uint64_t)__popc(word[k] & lt);
+                s_src[pos] = sv[k];
+                if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[k];
+            }
         }
     }
 }
@@ -220,7 +239,7 @@ uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, ui
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     const uint64_t pad = sparse_pad(g, kept);
     const size_t wb = weight_size(g.wkind);
-    const unsigned gr = grid_for(g.e_loc, 256, 148ull * 16 * 8);
+    const unsigned gr = grid_for((nwords + 7) / 8 * 32, 256, 148ull * 8);
     if (g.e_loc) {
         if (wb == 0)
             compact_kernel<0><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,

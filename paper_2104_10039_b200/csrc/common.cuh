@@ -122,6 +122,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
 // Streaming (read-once) 32-bit load: bypass L1, evict-first in L2.
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
     uint32_t v;
@@ -162,6 +165,55 @@ __device__ __forceinline__ M ld_msg(const M* p, uint64_t pol) {
 #pragma unroll
         for (int i = 0; i < (int)(sizeof(M) / 16); ++i)
             v[i] = ld_keep(reinterpret_cast<const uint4*>(p) + i, pol);
+        memcpy(&out, v, sizeof(M));
+    } else {
+        out = *p;
+    }
+    return out;
+}
+
+// Message gather with a per-lane choice of two fixed L2 policies: two
+// predicated loads whose policy operands stay warp-uniform (a per-lane
+// SELect of the policy costs a select + R2UR pair per gather).
+__device__ __forceinline__ uint32_t ld_keep2(const uint32_t* p, bool hot, uint64_t ph, uint64_t pc) {
+    uint32_t v;
+    asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n"
+        " @q ld.global.nc.L2::cache_hint.u32 %0, [%1], %3;\n"
+        " @!q ld.global.nc.L2::cache_hint.u32 %0, [%1], %4; }"
+        : "=r"(v) : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_keep2(const uint2* p, bool hot, uint64_t ph, uint64_t pc) {
+    uint2 v;
+    asm("{ .reg .pred q; setp.ne.u32 q, %3, 0;\n"
+        " @q ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %4;\n"
+        " @!q ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %5; }"
+        : "=r"(v.x), "=r"(v.y) : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_keep2(const uint4* p, bool hot, uint64_t ph, uint64_t pc) {
+    uint4 v;
+    asm("{ .reg .pred q; setp.ne.u32 q, %5, 0;\n"
+        " @q ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %6;\n"
+        " @!q ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %7; }"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
+    return v;
+}
+template <class M>
+__device__ __forceinline__ M ld_msg2(const M* p, bool hot, uint64_t ph, uint64_t pc) {
+    M out;
+    if constexpr (sizeof(M) == 4) {
+        uint32_t v = ld_keep2(reinterpret_cast<const uint32_t*>(p), hot, ph, pc);
+        memcpy(&out, &v, 4);
+    } else if constexpr (sizeof(M) == 8) {
+        uint2 v = ld_keep2(reinterpret_cast<const uint2*>(p), hot, ph, pc);
+        memcpy(&out, &v, 8);
+    } else if constexpr (sizeof(M) % 16 == 0) {
+        uint4 v[sizeof(M) / 16];
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(M) / 16); ++i)
+            v[i] = ld_keep2(reinterpret_cast<const uint4*>(p) + i, hot, ph, pc);
         memcpy(&out, v, sizeof(M));
     } else {
         out = *p;

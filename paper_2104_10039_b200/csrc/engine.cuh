@@ -100,6 +100,12 @@ struct Engine {
                                              g.num_sms);
         return cached;
     }
+    static int grid_stash(DevGraph& g) {
+        static int cached = 0;
+        if (!cached) cached = occupancy_grid((const void*)edge_pass2_stash_kernel<P, W>,
+                                             kBlockThreads, 0, g.num_sms);
+        return cached;
+    }
     static int grid_pass2(DevGraph& g) {
         static int cached = 0;
         if (!cached) cached = occupancy_grid((const void*)edge_pass2_kernel<P, W>, kBlockThreads, 0,
@@ -145,6 +151,24 @@ struct Engine {
         Acc* hv = ws.get<Acc>("hv", ntask_cap);
         Acc* tv = ws.get<Acc>("tv", ntask_cap);
         Acc* carry = ws.get<Acc>("carry", ntask_cap);
+        // superstep stash (see EdgeArgs::stash): one message per padded
+        // position of the full list + one prefix per run, when HBM allows
+        // (else pass 2 re-gathers).
+        Msg* stash = nullptr;
+        Acc* lane_pre = nullptr;
+        uint32_t* task_info = nullptr;
+        if (cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) {
+            const size_t sbytes = (g.full.e_end() + kRun) * sizeof(Msg);
+            const size_t pbytes = (g.full.nruns + 1) * sizeof(Acc);
+            const bool have = ws.bufs.count("stash") && ws.bufs["stash"].bytes >= sbytes;
+            size_t free_b = 0, total_b = 0;
+            if (!have) GGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (have || free_b > sbytes + pbytes + (4ull << 30)) {
+                stash = static_cast<Msg*>(ws.get("stash", sbytes));
+                lane_pre = ws.get<Acc>("lane_pre", g.full.nruns + 1);
+                task_info = ws.get<uint32_t>("task_info", g.full.ntasks + 1);
+            }
+        }
         const uint64_t nwords = (g.e_loc + 31) / 32;
         const size_t wsz = (size_t)weight_bytes<W>();
         uint32_t* bitmap = nullptr;
@@ -208,6 +232,9 @@ struct Engine {
             ea.hv = hv;
             ea.tv = tv;
             ea.carry = carry;
+            ea.stash = super ? stash : nullptr;
+            ea.lane_pre = lane_pre;
+            ea.task_info = task_info;
             ea.bitmap = bitmap;
             ea.theta = cfg.theta;
             VertexArgs<P, W> va{};
@@ -250,7 +277,10 @@ struct Engine {
             ++launches;
             if (timing) GGB_CUDA(cudaEventRecord(e2, g.stream));
             if (super && L.ntasks) {  // flags of vertices whose fold began in an earlier task
-                edge_pass2_kernel<P, W><<<grid_pass2(g), kBlockThreads, 0, g.stream>>>(ea);
+                if (stash)
+                    edge_pass2_stash_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
+                else
+                    edge_pass2_kernel<P, W><<<grid_pass2(g), kBlockThreads, 0, g.stream>>>(ea);
                 GGB_CUDA(cudaGetLastError());
                 ++launches;
             }

@@ -82,6 +82,13 @@ struct EdgeArgs {
     typename P::Accum* __restrict__ hv;       // [task] continuing head piece
     typename P::Accum* __restrict__ tv;       // [task] continuing tail piece
     const typename P::Accum* __restrict__ carry;  // [task] pass 2: carry into the task
+    // superstep stash (nullable): pass 1 saves, for the lanes of each task's
+    // continuing first vertex, the run's gathered messages ([padded position])
+    // and the lane's exclusive in-task prefix ([run]); pass 2 then streams
+    // them instead of re-gathering.
+    typename P::Message* __restrict__ stash;
+    typename P::Accum* __restrict__ lane_pre;
+    uint32_t* __restrict__ task_info;  // [task] kTaskCont | kTaskProc | end of the first vertex
     uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
     double theta;
 };
@@ -110,6 +117,28 @@ struct VertexArgs {
 
 __device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t v) {
     return (st[v] & kStActive) || a_off[v + 1] > a_off[v];  // engine.hpp:196
+}
+
+// Fold loops are fully unrolled (messages stay in registers) unless the
+// program's gather is long (BP: three f64 divisions and two passes over the
+// states), where 2 x 16 inlined copies thrash the instruction cache; those
+// loops run rolled over a local-memory message array.
+template <class P>
+__host__ __device__ constexpr int fold_unroll() {
+    if constexpr (requires { P::kHeavyGather; }) return P::kHeavyGather ? 1 : kRun;
+    else return kRun;
+}
+// f(j) for j = 0..kRun-1, unrolled per fold_unroll (a plain `#pragma unroll`
+// for light programs: an explicit count changes ptxas's allocation).
+template <class P, class F>
+__device__ __forceinline__ void for_run(F&& f) {
+    if constexpr (fold_unroll<P>() == 1) {
+#pragma unroll 1
+        for (int j = 0; j < kRun; ++j) f(j);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) f(j);
+    }
 }
 
 template <class W>
@@ -145,8 +174,34 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
     // inside the padded allocation.
 #pragma unroll
     for (int j = 0; j < kRun; ++j) {
-        m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
+        if constexpr (fold_unroll<P>() != 1)
+            m[j] = ld_msg2(a.msg_cur + s[j], s[j] < a.hot_limit, pol_hot, pol_cold);
+        else
+            m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
         if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + P0 + j);
+    }
+}
+
+// task_info word written by superstep pass 1 for the stash pass 2
+constexpr uint32_t kTaskCont = 1u << 16;  // the first vertex began in an earlier task
+constexpr uint32_t kTaskProc = 1u << 17;  // ... and is processed this iteration
+
+// Rewrite the flags this lane owns (bits of `own`, relative to P0) to
+// `kbits`; flags of edges of skipped vertices persist (engine.hpp:204-211).
+__device__ __forceinline__ void write_flags(uint32_t* __restrict__ bitmap, uint64_t pad,
+                                            uint64_t P0, uint64_t lo, uint32_t own,
+                                            uint32_t kbits) {
+    if (!own) return;
+    const uint64_t e0 = lo - pad;  // local edge id of bit (lo - P0)
+    const uint32_t shift_in = (uint32_t)(lo - P0);
+    const uint32_t O = own >> shift_in, K = kbits >> shift_in;
+    const uint32_t sh = (uint32_t)(e0 & 31);
+    const uint64_t K64 = (uint64_t)K << sh, O64 = (uint64_t)O << sh;
+    uint32_t* wp = bitmap + (e0 >> 5);
+    if ((uint32_t)O64) { atomicAnd(wp, ~(uint32_t)O64); atomicOr(wp, (uint32_t)K64); }
+    if ((uint32_t)(O64 >> 32)) {
+        atomicAnd(wp + 1, ~(uint32_t)(O64 >> 32));
+        atomicOr(wp + 1, (uint32_t)(K64 >> 32));
     }
 }
 
@@ -158,11 +213,34 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     using Message = typename P::Message;
     constexpr bool SUPER = MODE == kEdgeSuper;
     const uint64_t tstart = t * kChunkEdges;
+    const uint64_t r = t * kWarp + lane;
+    const uint64_t P0 = r * kRun;
+    const uint64_t lo = P0 > a.pad ? P0 : a.pad;
+    uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
     // non-empty vertices touching the task: [i0, i_next], starts staged
     const uint32_t i0 = a.run_i[t * kWarp];
-    const uint64_t rn = (t + 1) * kWarp;
-    const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
-    const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
+    Message m[kRun];
+    WStore<W> wr[kRun];
+    int len = 0;
+    uint32_t ri = 0;  // run_i[r]: the non-empty vertex at the run's first position
+    // Sources and message gathers do not depend on the staged starts: for
+    // register-resident runs issue them first so their latency overlaps the
+    // staging loads (local-memory runs of heavy programs measured better
+    // the other way round).
+    constexpr bool kEarly = !PASS2 && fold_unroll<P>() != 1;
+    if constexpr (kEarly) {
+        len = hi > lo ? (int)(hi - lo) : 0;
+        if (len > 0) {
+            ri = a.run_i[r];
+            load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
+        }
+    }
+    uint32_t cnt = 2;  // pass 2 only needs the first vertex's start and end
+    if constexpr (!PASS2) {
+        const uint64_t rn = (t + 1) * kWarp;
+        const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
+        cnt = i_next - i0 + 2;  // <= kStageStarts
+    }
     for (uint32_t j = lane; j < cnt; j += kWarp) {
         const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
         st0[j] = (int16_t)(rel < 0 ? -1 : (rel > kChunkEdges ? kChunkEdges + 1 : rel));
@@ -170,20 +248,18 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     __syncwarp();
     const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
     if (PASS2 && !cont) return;    // warp-uniform
-    const uint64_t r = t * kWarp + lane;
-    const uint64_t P0 = r * kRun;
-    const uint64_t lo = P0 > a.pad ? P0 : a.pad;
-    uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
     if constexpr (PASS2) {  // pass 2 only re-walks the continuing first vertex's edges
         const uint64_t vend = tstart + (uint64_t)(st0[1] > 0 ? st0[1] : 0);
         if (hi > vend) hi = vend;
     }
-    const int len = hi > lo ? (int)(hi - lo) : 0;
+    if constexpr (!kEarly) {
+        len = hi > lo ? (int)(hi - lo) : 0;
+        if (len > 0) {
+            ri = a.run_i[r];
+            load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
+        }
+    }
     const int rlo = (int)(lo - tstart), rhi = (int)(hi - tstart);  // task-relative
-
-    Message m[kRun];
-    WStore<W> wr[kRun];
-    if (len > 0) load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
     auto wv = [&](int j) -> double {
         if constexpr (std::is_void_v<W>) return 1.0;
         else return (double)wr[j];
@@ -191,7 +267,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
 
     // sequential fold of the run, closing the vertices that end inside it
     // (k: index relative to i0; nb: task-relative end of vertex k)
-    int k = len > 0 ? (int)(a.run_i[r] - i0) : 0;
+    int k = len > 0 ? (int)(ri - i0) : 0;
     const int hk = k;
     int nb = len > 0 ? st0[k + 1] : 0;
     bool pk = true;
@@ -200,8 +276,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
     Accum x = a.prog.gather_identity(), hvv = x;
     bool head_closed = false;
-#pragma unroll
-    for (int j = 0; j < kRun; ++j) {
+    for_run<P>([&](int j) {
         const int p = (int)(P0 - tstart) + j;
         if (p >= rlo && p < rhi) {
             if (p >= nb) {  // vertex k ended before p: next non-empty vertex
@@ -222,7 +297,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 pmask |= 1u << j;
             }
         }
-    }
+    });
     const uint32_t tk = len > 0 ? (uint32_t)k : 0x7fffff00u + (uint32_t)lane;  // unique when empty
     // join runs sharing a destination: segmented inclusive scan keyed by tk
     Accum S = x;
@@ -256,11 +331,22 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         // influence of each edge against its exclusive running prefix
         // (engine.hpp:204-211); a vertex whose fold began in an earlier task
         // is handled by pass 2 with that task's carry.
+        if (!PASS2 && a.stash && lane == 0)  // lane 0's first position is the task start
+            a.task_info[t] = cont ? (kTaskCont | ((pmask & 1u) ? kTaskProc : 0u) | (uint32_t)st0[1])
+                                  : 0u;
         Accum run = a.prog.gather_identity();
         bool skip_head = false;
         if (cont && hk == 0) {
-            if (PASS2) run = a.carry[t];
-            else skip_head = true;
+            if (PASS2) {
+                run = a.carry[t];
+            } else {
+                skip_head = true;
+                if (a.stash && len > 0) {  // hand the head vertex's edges to pass 2
+                    a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
+#pragma unroll
+                    for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
+                }
+            }
         } else if (PASS2) {
             skip_head = true;  // pass 2 only rewrites the continuing vertex
         }
@@ -269,8 +355,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         int nb2 = len > 0 ? st0[hk + 1] : 0;
         int kk = hk;
         bool in_head = true;
-#pragma unroll
-        for (int j = 0; j < kRun; ++j) {
+        for_run<P>([&](int j) {
             const int p = (int)(P0 - tstart) + j;
             if (p >= rlo && p < rhi) {
                 if (p >= nb2) {
@@ -287,21 +372,8 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
                 }
             }
-        }
-        if (own) {
-            const uint64_t e0 = lo - a.pad;  // local edge id of bit (lo - P0)
-            const uint32_t shift_in = (uint32_t)(lo - P0);
-            const uint32_t O = own >> shift_in, K = kbits >> shift_in;
-            const uint32_t sh = (uint32_t)(e0 & 31);
-            const uint64_t K64 = (uint64_t)K << sh, O64 = (uint64_t)O << sh;
-            uint32_t* wp = a.bitmap + (e0 >> 5);
-            // flags of edges of skipped vertices persist (SPEC: superstep scope)
-            if ((uint32_t)O64) { atomicAnd(wp, ~(uint32_t)O64); atomicOr(wp, (uint32_t)K64); }
-            if ((uint32_t)(O64 >> 32)) {
-                atomicAnd(wp + 1, ~(uint32_t)(O64 >> 32));
-                atomicOr(wp + 1, (uint32_t)(K64 >> 32));
-            }
-        }
+        });
+        write_flags(a.bitmap, a.pad, P0, lo, own, kbits);
     }
     __syncwarp();  // st0 is restaged by the warp's next task
 }
@@ -316,9 +388,10 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t pol_cold = policy_evict_normal();
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
-         t += warps)
+         t += warps) {
         edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
                               pol_cold);
+    }
 }
 
 template <class P, class W>
@@ -334,6 +407,46 @@ edge_pass2_kernel(const EdgeArgs<P, W> a) {
          t += warps)
         edge_task<P, W, kEdgeSuper, true>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream,
                                     pol_hot, pol_cold);
+}
+
+// Superstep pass 2 from the stash: for every task whose first vertex began
+// in an earlier task, that vertex's flags in this task, from
+//   carry[t] (+) lane_pre[r], then the run's own sequential gathers
+// over the stashed messages -- the same arithmetic as the re-gathering pass 2
+// (combine with the identity is exact), with no source or message reads.
+template <class P, class W>
+__global__ void __launch_bounds__(kBlockThreads)
+edge_pass2_stash_kernel(const EdgeArgs<P, W> a) {
+    using Accum = typename P::Accum;
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
+    for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
+         t += warps) {
+        const uint64_t tstart = t * kChunkEdges;
+        const uint32_t info = a.task_info[t];
+        // warp-uniform: no continuing vertex, or a skipped one (its flags persist)
+        if ((info & (kTaskCont | kTaskProc)) != (kTaskCont | kTaskProc)) continue;
+        const uint64_t vend = tstart + (info & 0xffffu);
+        const uint64_t r = t * kWarp + lane;
+        const uint64_t P0 = r * kRun;
+        const uint64_t lo = P0;  // > pad: the task does not hold list position 0
+        uint64_t hi = P0 + kRun;
+        if (hi > vend) hi = vend;
+        if (hi <= lo) continue;
+        Accum run = a.prog.combine(a.carry[t], a.lane_pre[r]);
+        uint32_t kbits = 0, own = 0;
+        for_run<P>([&](int j) {
+            const uint64_t p = P0 + j;
+            if (p < hi) {
+                double w = 1.0;
+                if constexpr (!std::is_void_v<W>) w = (double)a.w[p];
+                const double infl = a.prog.gather(run, a.stash[p], w);
+                if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
+                own |= 1u << j;
+            }
+        });
+        write_flags(a.bitmap, a.pad, P0, lo, own, kbits);
+    }
 }
 
 // Vertex epilogue: the accumulator of vertex v is acc_out[v] when its list

@@ -225,6 +225,7 @@ struct BeliefProp {
     using Accum = Belief<S>;
     static constexpr bool kMsgIsProp = true;
     static constexpr bool kNeedsDegree = false;
+    static constexpr bool kHeavyGather = true;
     double coupling = 0.8, epsilon = 1e-6;
 
     __device__ Property prior(uint32_t v) const {  // algorithms.cpp:9-23
@@ -288,6 +289,7 @@ struct BeliefPropEdge {
     static constexpr bool kMsgIsProp = true;
     static constexpr bool kNeedsDegree = false;
     static constexpr bool kReadsPrior = true;
+    static constexpr bool kHeavyGather = true;
     const float2* prior_table = nullptr;
     double epsilon = 1e-6;
 
