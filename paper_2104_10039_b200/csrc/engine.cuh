@@ -102,7 +102,7 @@ struct Engine {
     }
     static int grid_stash(DevGraph& g) {
         static int cached = 0;
-        if (!cached) cached = occupancy_grid((const void*)edge_pass2_stash_kernel<P, W>,
+        if (!cached) cached = occupancy_grid((const void*)edge_influence_kernel<P, W>,
                                              kBlockThreads, 0, g.num_sms);
         return cached;
     }
@@ -157,8 +157,9 @@ struct Engine {
         Msg* stash = nullptr;
         Acc* lane_pre = nullptr;
         uint32_t* task_info = nullptr;
+        uint32_t* run_meta = nullptr;
         if (cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) {
-            const size_t sbytes = (g.full.e_end() + kRun) * sizeof(Msg);
+            const size_t sbytes = (g.full.ntasks * kChunkEdges + kRun) * sizeof(Msg);
             const size_t pbytes = (g.full.nruns + 1) * sizeof(Acc);
             const bool have = ws.bufs.count("stash") && ws.bufs["stash"].bytes >= sbytes;
             size_t free_b = 0, total_b = 0;
@@ -167,6 +168,7 @@ struct Engine {
                 stash = static_cast<Msg*>(ws.get("stash", sbytes));
                 lane_pre = ws.get<Acc>("lane_pre", g.full.nruns + 1);
                 task_info = ws.get<uint32_t>("task_info", g.full.ntasks + 1);
+                run_meta = ws.get<uint32_t>("run_meta", g.full.nruns + 1);
             }
         }
         const uint64_t nwords = (g.e_loc + 31) / 32;
@@ -234,6 +236,7 @@ struct Engine {
             ea.carry = carry;
             ea.stash = super ? stash : nullptr;
             ea.lane_pre = lane_pre;
+            ea.run_meta = run_meta;
             ea.task_info = task_info;
             ea.bitmap = bitmap;
             ea.theta = cfg.theta;
@@ -265,7 +268,8 @@ struct Engine {
                 // every edge of the sparsified list (and of the full list under
                 // the accurate scheme) belongs to a processed vertex
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
-                if (super) launch_edge<kEdgeSuper>(g, ea);
+                if (super && stash) launch_edge<kEdgeFoldStash>(g, ea);
+                else if (super) launch_edge<kEdgeSuper>(g, ea);
                 else if (all_proc) launch_edge<kEdgePlain>(g, ea);
                 else launch_edge<kEdgeCheck>(g, ea);
                 ++launches;
@@ -278,7 +282,7 @@ struct Engine {
             if (timing) GGB_CUDA(cudaEventRecord(e2, g.stream));
             if (super && L.ntasks) {  // flags of vertices whose fold began in an earlier task
                 if (stash)
-                    edge_pass2_stash_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
+                    edge_influence_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
                 else
                     edge_pass2_kernel<P, W><<<grid_pass2(g), kBlockThreads, 0, g.stream>>>(ea);
                 GGB_CUDA(cudaGetLastError());

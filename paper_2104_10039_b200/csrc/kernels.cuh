@@ -58,6 +58,9 @@ enum : int {
     kEdgePlain = 0,  // every edge of the list belongs to a processed vertex
     kEdgeCheck = 1,  // full list, skip edges of unprocessed vertices
     kEdgeSuper = 2,  // superstep: + influence / estatus into the bitmap
+    kEdgeFoldStash = 3,  // superstep pass 1 of the stash scheme: fold + hand every
+                         // run's messages, prefix and vertex marks to the
+                         // influence pass (edge_influence_kernel)
 };
 
 // non-empty vertex starts of one task, relative to the task start, clamped
@@ -82,13 +85,15 @@ struct EdgeArgs {
     typename P::Accum* __restrict__ hv;       // [task] continuing head piece
     typename P::Accum* __restrict__ tv;       // [task] continuing tail piece
     const typename P::Accum* __restrict__ carry;  // [task] pass 2: carry into the task
-    // superstep stash (nullable): pass 1 saves, for the lanes of each task's
-    // continuing first vertex, the run's gathered messages ([padded position])
-    // and the lane's exclusive in-task prefix ([run]); pass 2 then streams
-    // them instead of re-gathering.
+    // superstep stash (kEdgeFoldStash -> edge_influence_kernel): pass 1
+    // saves every run's gathered messages ([padded position]), the lane's
+    // exclusive in-task prefix of its first vertex ([run]) and its vertex
+    // marks ([run]: bits 0-15 a vertex starts at P0+j, bits 16-31 the edge
+    // belongs to a processed vertex); the influence pass streams them.
     typename P::Message* __restrict__ stash;
     typename P::Accum* __restrict__ lane_pre;
-    uint32_t* __restrict__ task_info;  // [task] kTaskCont | kTaskProc | end of the first vertex
+    uint32_t* __restrict__ run_meta;
+    uint32_t* __restrict__ task_info;  // [task] kTaskCont | end of the first vertex
     uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
     double theta;
 };
@@ -141,6 +146,15 @@ __device__ __forceinline__ void for_run(F&& f) {
     }
 }
 
+// Stash rows go through WarpRows (coalesced 512-byte accesses) when a run's
+// messages form a power-of-two number of 16-byte chunks that fits 8 KB of
+// shared memory per warp; otherwise lanes store / load their runs directly.
+template <class P>
+__host__ __device__ constexpr int stash_row_bytes() {
+    constexpr int b = (int)sizeof(typename P::Message) * kRun;
+    return (b % 16 == 0 && ((b / 16) & (b / 16 - 1)) == 0 && b <= 256) ? b : 0;
+}
+
 template <class W>
 using WStore = std::conditional_t<std::is_void_v<W>, char, W>;
 
@@ -182,9 +196,9 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
     }
 }
 
-// task_info word written by superstep pass 1 for the stash pass 2
+// task_info word written by the stash pass 1 (low 16 bits: task-relative
+// end of the task's first vertex, clamped to 513)
 constexpr uint32_t kTaskCont = 1u << 16;  // the first vertex began in an earlier task
-constexpr uint32_t kTaskProc = 1u << 17;  // ... and is processed this iteration
 
 // Rewrite the flags this lane owns (bits of `own`, relative to P0) to
 // `kbits`; flags of edges of skipped vertices persist (engine.hpp:204-211).
@@ -206,8 +220,8 @@ __device__ __forceinline__ void write_flags(uint32_t* __restrict__ bitmap, uint6
 }
 
 template <class P, class W, int MODE, bool PASS2>
-__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint64_t t,
-                                          int lane, uint64_t pol_stream,
+__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, char* xs,
+                                          uint64_t t, int lane, uint64_t pol_stream,
                                           uint64_t pol_hot, uint64_t pol_cold) {
     using Accum = typename P::Accum;
     using Message = typename P::Message;
@@ -274,6 +288,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     if constexpr (MODE != kEdgePlain)
         if (len > 0) pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
+    uint32_t bmask = 0;  // positions where a later vertex of the run starts
     Accum x = a.prog.gather_identity(), hvv = x;
     bool head_closed = false;
     for_run<P>([&](int j) {
@@ -289,6 +304,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 x = a.prog.gather_identity();
                 ++k;
                 nb = st0[k + 1];
+                if constexpr (MODE == kEdgeFoldStash) bmask |= 1u << j;
                 if constexpr (MODE != kEdgePlain)
                     pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
             }
@@ -331,22 +347,11 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         // influence of each edge against its exclusive running prefix
         // (engine.hpp:204-211); a vertex whose fold began in an earlier task
         // is handled by pass 2 with that task's carry.
-        if (!PASS2 && a.stash && lane == 0)  // lane 0's first position is the task start
-            a.task_info[t] = cont ? (kTaskCont | ((pmask & 1u) ? kTaskProc : 0u) | (uint32_t)st0[1])
-                                  : 0u;
         Accum run = a.prog.gather_identity();
         bool skip_head = false;
         if (cont && hk == 0) {
-            if (PASS2) {
-                run = a.carry[t];
-            } else {
-                skip_head = true;
-                if (a.stash && len > 0) {  // hand the head vertex's edges to pass 2
-                    a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
-#pragma unroll
-                    for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
-                }
-            }
+            if (PASS2) run = a.carry[t];
+            else skip_head = true;
         } else if (PASS2) {
             skip_head = true;  // pass 2 only rewrites the continuing vertex
         }
@@ -375,6 +380,21 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         });
         write_flags(a.bitmap, a.pad, P0, lo, own, kbits);
     }
+    if constexpr (MODE == kEdgeFoldStash) {
+        if (lane == 0) a.task_info[t] = cont ? (kTaskCont | (uint32_t)st0[1]) : 0u;
+        a.run_meta[r] = len > 0 ? (bmask | (pmask << 16)) : 0u;
+        if (pmask) a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
+        constexpr int RB = stash_row_bytes<P>();
+        if constexpr (RB != 0) {  // warp-collective, coalesced
+            uint4 row[RB / 16];
+            memcpy(row, m, RB);
+            WarpRows<RB>::store(xs, lane, row,
+                                reinterpret_cast<uint4*>(a.stash + t * kChunkEdges));
+        } else if (pmask) {
+#pragma unroll
+            for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
+        }
+    }
     __syncwarp();  // st0 is restaged by the warp's next task
 }
 
@@ -382,6 +402,8 @@ template <class P, class W, int MODE>
 __global__ void __launch_bounds__(kBlockThreads)
 edge_kernel(const EdgeArgs<P, W> a) {
     __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
+    constexpr int RB = MODE == kEdgeFoldStash ? stash_row_bytes<P>() : 0;
+    __shared__ __align__(16) char xs_all[kWarpsPerBlock][RB ? 32 * RB : 16];
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
@@ -389,8 +411,8 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
-        edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
-                              pol_cold);
+        edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], xs_all[threadIdx.x >> 5], t,
+                                     lane, pol_stream, pol_hot, pol_cold);
     }
 }
 
@@ -405,47 +427,63 @@ edge_pass2_kernel(const EdgeArgs<P, W> a) {
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
-        edge_task<P, W, kEdgeSuper, true>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream,
-                                    pol_hot, pol_cold);
+        edge_task<P, W, kEdgeSuper, true>(a, st_all[threadIdx.x >> 5], nullptr, t, lane,
+                                          pol_stream, pol_hot, pol_cold);
 }
 
-// Superstep pass 2 from the stash: for every task whose first vertex began
-// in an earlier task, that vertex's flags in this task, from
-//   carry[t] (+) lane_pre[r], then the run's own sequential gathers
-// over the stashed messages -- the same arithmetic as the re-gathering pass 2
-// (combine with the identity is exact), with no source or message reads.
+// Superstep influence pass of the stash scheme (engine.hpp:204-211): every
+// edge of a processed vertex gets estatus(gather(prefix, message)) with the
+// prefix = the accumulator before the edge in CSC order:
+//   run's first vertex, continuing from an earlier task: carry[t] (+) lane_pre[r]
+//   run's first vertex otherwise:                       lane_pre[r]
+//   later vertices of the run:                          identity at their start
+// then the run's own sequential gathers over the stashed messages -- the
+// arithmetic of the single-kernel superstep (combine with the identity is
+// exact), as a pure stream: no sources, no message gathers, no staging.
 template <class P, class W>
 __global__ void __launch_bounds__(kBlockThreads)
-edge_pass2_stash_kernel(const EdgeArgs<P, W> a) {
+edge_influence_kernel(const EdgeArgs<P, W> a) {
     using Accum = typename P::Accum;
+    using Message = typename P::Message;
+    constexpr int RB = stash_row_bytes<P>();
+    __shared__ __align__(16) char xs_all[kWarpsPerBlock][RB ? 32 * RB : 16];
+    char* xs = xs_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
-        const uint64_t tstart = t * kChunkEdges;
-        const uint32_t info = a.task_info[t];
-        // warp-uniform: no continuing vertex, or a skipped one (its flags persist)
-        if ((info & (kTaskCont | kTaskProc)) != (kTaskCont | kTaskProc)) continue;
-        const uint64_t vend = tstart + (info & 0xffffu);
         const uint64_t r = t * kWarp + lane;
+        const uint32_t meta = a.run_meta[r];
+        const uint32_t own = meta >> 16;
+        if (!__any_sync(0xffffffffu, own != 0)) continue;  // warp-uniform
+        const uint32_t info = a.task_info[t];
         const uint64_t P0 = r * kRun;
-        const uint64_t lo = P0;  // > pad: the task does not hold list position 0
-        uint64_t hi = P0 + kRun;
-        if (hi > vend) hi = vend;
-        if (hi <= lo) continue;
-        Accum run = a.prog.combine(a.carry[t], a.lane_pre[r]);
-        uint32_t kbits = 0, own = 0;
+        Message mm[kRun];
+        if constexpr (RB != 0) {
+            uint4 row[RB / 16];
+            WarpRows<RB>::load(xs, lane, reinterpret_cast<const uint4*>(a.stash + t * kChunkEdges),
+                               row);
+            memcpy(mm, row, RB);
+        } else {
+            if (own) {
+#pragma unroll
+                for (int j = 0; j < kRun; ++j) mm[j] = a.stash[P0 + j];
+            }
+        }
+        if (!own) continue;
+        const bool head = (info & kTaskCont) && P0 < t * kChunkEdges + (info & 0xffffu);
+        Accum run = a.prog.combine(head ? a.carry[t] : a.prog.gather_identity(), a.lane_pre[r]);
+        uint32_t kbits = 0;
         for_run<P>([&](int j) {
-            const uint64_t p = P0 + j;
-            if (p < hi) {
+            if ((meta >> j) & 1u) run = a.prog.gather_identity();
+            if ((own >> j) & 1u) {
                 double w = 1.0;
-                if constexpr (!std::is_void_v<W>) w = (double)a.w[p];
-                const double infl = a.prog.gather(run, a.stash[p], w);
+                if constexpr (!std::is_void_v<W>) w = (double)a.w[P0 + j];
+                const double infl = a.prog.gather(run, mm[j], w);
                 if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
-                own |= 1u << j;
             }
         });
-        write_flags(a.bitmap, a.pad, P0, lo, own, kbits);
+        write_flags(a.bitmap, a.pad, P0, P0 > a.pad ? P0 : a.pad, own, kbits);
     }
 }
 
