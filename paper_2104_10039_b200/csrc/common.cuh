@@ -178,7 +178,7 @@ __device__ __forceinline__ M ld_msg(const M* p, uint64_t pol) {
 __device__ __forceinline__ uint32_t ld_keep2(const uint32_t* p, bool hot, uint64_t ph, uint64_t pc) {
     uint32_t v;
     asm("{ .reg .pred q; setp.ne.u32 q, %2, 0;\n"
-        " @q ld.global.nc.L2::cache_hint.u32 %0, [%1], %3;\n"
+        " @q ld.global.nc.L1::evict_last.L2::cache_hint.u32 %0, [%1], %3;\n"
         " @!q ld.global.nc.L2::cache_hint.u32 %0, [%1], %4; }"
         : "=r"(v) : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
     return v;
@@ -186,7 +186,7 @@ __device__ __forceinline__ uint32_t ld_keep2(const uint32_t* p, bool hot, uint64
 __device__ __forceinline__ uint2 ld_keep2(const uint2* p, bool hot, uint64_t ph, uint64_t pc) {
     uint2 v;
     asm("{ .reg .pred q; setp.ne.u32 q, %3, 0;\n"
-        " @q ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %4;\n"
+        " @q ld.global.nc.L1::evict_last.L2::cache_hint.v2.u32 {%0, %1}, [%2], %4;\n"
         " @!q ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %5; }"
         : "=r"(v.x), "=r"(v.y) : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
     return v;
@@ -194,7 +194,7 @@ __device__ __forceinline__ uint2 ld_keep2(const uint2* p, bool hot, uint64_t ph,
 __device__ __forceinline__ uint4 ld_keep2(const uint4* p, bool hot, uint64_t ph, uint64_t pc) {
     uint4 v;
     asm("{ .reg .pred q; setp.ne.u32 q, %5, 0;\n"
-        " @q ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %6;\n"
+        " @q ld.global.nc.L1::evict_last.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %6;\n"
         " @!q ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %7; }"
         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
         : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));

@@ -80,7 +80,13 @@ struct EdgeArgs {
     const uint64_t* __restrict__ a_off;     // active_in_degree offsets (engine.hpp:154-161)
     const uint8_t* __restrict__ st_cur;
     const typename P::Message* __restrict__ msg_cur;  // global ids
-    uint32_t hot_limit;                     // sources below this id: L2 evict_last
+    // Message-gather cache classes (hot-first slots: low ids are the most read):
+    //   slot < hot_limit: L1 evict_last + L2 evict_last   (register-resident runs)
+    //   slot < l2_limit:  L2 evict_last                    (heavy programs' runs)
+    //   otherwise:        L2 evict_last if cold_last, else evict_normal
+    uint32_t hot_limit;
+    uint32_t l2_limit;
+    uint32_t cold_last;
     typename P::Accum* __restrict__ acc_out;  // [local vertex]
     typename P::Accum* __restrict__ hv;       // [task] continuing head piece
     typename P::Accum* __restrict__ tv;       // [task] continuing tail piece
@@ -191,7 +197,7 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
         if constexpr (fold_unroll<P>() != 1)
             m[j] = ld_msg2(a.msg_cur + s[j], s[j] < a.hot_limit, pol_hot, pol_cold);
         else
-            m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.hot_limit ? pol_hot : pol_cold);
+            m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.l2_limit ? pol_hot : pol_cold);
         if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + P0 + j);
     }
 }
@@ -407,7 +413,7 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
-    const uint64_t pol_cold = policy_evict_normal();
+    const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
@@ -423,7 +429,7 @@ edge_pass2_kernel(const EdgeArgs<P, W> a) {
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
-    const uint64_t pol_cold = policy_evict_normal();
+    const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
