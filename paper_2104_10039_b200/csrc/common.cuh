@@ -241,7 +241,7 @@ struct WarpRows {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             const int c = i * 32 + lane;
-            gdst[c] = *reinterpret_cast<const uint4*>(xs + at(c / Q, c % Q));
+            __stcs(gdst + c, *reinterpret_cast<const uint4*>(xs + at(c / Q, c % Q)));  // streaming: keep L2 for gathers
         }
         __syncwarp();
     }

@@ -388,7 +388,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     }
     if constexpr (MODE == kEdgeFoldStash) {
         if (lane == 0) a.task_info[t] = cont ? (kTaskCont | (uint32_t)st0[1]) : 0u;
-        a.run_meta[r] = len > 0 ? (bmask | (pmask << 16)) : 0u;
+        __stcs(a.run_meta + r, len > 0 ? (bmask | (pmask << 16)) : 0u);
         if (pmask) a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
         constexpr int RB = stash_row_bytes<P>();
         if constexpr (RB != 0) {  // warp-collective, coalesced
