@@ -22,7 +22,10 @@ constexpr int kWindow = 32;              // vertices per window (one per lane)
 constexpr int kRun = 16;                 // consecutive in-edges folded by one lane
 constexpr int kChunkEdges = kWarp * kRun;  // in-edges per warp task (512)
 constexpr int kRowsPerChunk = kChunkEdges / 32;
-constexpr int kBlockThreads = 128;
+#ifndef GGB_EDGE_BLOCK_THREADS
+#define GGB_EDGE_BLOCK_THREADS 128
+#endif
+constexpr int kBlockThreads = GGB_EDGE_BLOCK_THREADS;
 constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 
 // splitmix64 finalizer: engine.cpp:9-14 (bit-identical on host and device).
@@ -200,6 +203,56 @@ __device__ __forceinline__ uint4 ld_keep2(const uint4* p, bool hot, uint64_t ph,
         : "l"(p), "r"((uint32_t)hot), "l"(ph), "l"(pc));
     return v;
 }
+// Three-way message gather: class 0 from a shared-memory copy of the hot
+// slots (saddr), 1 = global with L1+L2 evict_last, 2 = global with policy pc.
+#define GGB_LDS3(VEC, OUTS, SADDR, GADDR, CLS, PH, PC)                                   \
+    "{ .reg .pred q0, q1, q2;\n"                                                          \
+    " setp.eq.u32 q0, " CLS ", 0; setp.eq.u32 q1, " CLS ", 1; setp.eq.u32 q2, " CLS ", 2;\n" \
+    " @q0 ld.shared" VEC " " OUTS ", [" SADDR "];\n"                                      \
+    " @q1 ld.global.nc.L1::evict_last.L2::cache_hint" VEC " " OUTS ", [" GADDR "], " PH ";\n" \
+    " @q2 ld.global.nc.L2::cache_hint" VEC " " OUTS ", [" GADDR "], " PC "; }"
+__device__ __forceinline__ uint32_t ld_hot3(const uint32_t* p, uint32_t sa, uint32_t cls, uint64_t ph,
+                                            uint64_t pc) {
+    uint32_t v;
+    asm(GGB_LDS3(".u32", "%0", "%1", "%2", "%3", "%4", "%5")
+        : "=r"(v) : "r"(sa), "l"(p), "r"(cls), "l"(ph), "l"(pc));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_hot3(const uint2* p, uint32_t sa, uint32_t cls, uint64_t ph,
+                                         uint64_t pc) {
+    uint2 v;
+    asm(GGB_LDS3(".v2.u32", "{%0, %1}", "%2", "%3", "%4", "%5", "%6")
+        : "=r"(v.x), "=r"(v.y) : "r"(sa), "l"(p), "r"(cls), "l"(ph), "l"(pc));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_hot3(const uint4* p, uint32_t sa, uint32_t cls, uint64_t ph,
+                                         uint64_t pc) {
+    uint4 v;
+    asm(GGB_LDS3(".v4.u32", "{%0, %1, %2, %3}", "%4", "%5", "%6", "%7", "%8")
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(sa), "l"(p), "r"(cls), "l"(ph), "l"(pc));
+    return v;
+}
+#undef GGB_LDS3
+template <class M>
+__device__ __forceinline__ M ld_msg_hot(const M* p, uint32_t sa, uint32_t cls, uint64_t ph, uint64_t pc) {
+    M out;
+    if constexpr (sizeof(M) == 4) {
+        uint32_t v = ld_hot3(reinterpret_cast<const uint32_t*>(p), sa, cls, ph, pc);
+        memcpy(&out, &v, 4);
+    } else if constexpr (sizeof(M) == 8) {
+        uint2 v = ld_hot3(reinterpret_cast<const uint2*>(p), sa, cls, ph, pc);
+        memcpy(&out, &v, 8);
+    } else {
+        static_assert(sizeof(M) % 16 == 0, "message size");
+        uint4 v[sizeof(M) / 16];
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(M) / 16); ++i)
+            v[i] = ld_hot3(reinterpret_cast<const uint4*>(p) + i, sa + 16 * i, cls, ph, pc);
+        memcpy(&out, v, sizeof(M));
+    }
+    return out;
+}
+
 template <class M>
 __device__ __forceinline__ M ld_msg2(const M* p, bool hot, uint64_t ph, uint64_t pc) {
     M out;

@@ -137,6 +137,34 @@ struct Engine {
         return nloc * bv;
     }
 
+    // shared-memory hot-slot table of edge_kernel_hot (GGB_SMEM_HOT_KB, default
+    // 160 KB; 0 disables the hot kernel)
+    static constexpr bool kHotOK =
+        fold_unroll<P>() != 1 && (sizeof(Msg) == 4 || sizeof(Msg) == 8 || sizeof(Msg) == 16);
+    // Measured (approximate gather, one B200): 4-byte messages gain 18% (c3
+    // WCC) / 5% (c2 SSSP) with a 64 KB table; 8-byte PageRank messages lose
+    // at every size (the L1 evict_last class already holds their hot lines
+    // and the 24-warp CTA spills), so the table is off for them.
+    static size_t smem_hot_bytes() {
+        static size_t b = [] {
+            const char* e = std::getenv("GGB_SMEM_HOT_KB");
+            return (size_t)(e ? std::atol(e) : (sizeof(Msg) == 4 ? 64 : 0)) << 10;
+        }();
+        return b;
+    }
+    static void launch_edge_hot(DevGraph& g, const EdgeArgs<P, W>& ea, uint32_t nhot) {
+        static bool attr = false;
+        const size_t bytes = (size_t)nhot * sizeof(Msg);
+        if (!attr) {
+            GGB_CUDA(cudaFuncSetAttribute((const void*)edge_kernel_hot<P, W, kEdgePlain>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)std::max<size_t>(smem_hot_bytes(), 16)));
+            attr = true;
+        }
+        edge_kernel_hot<P, W, kEdgePlain><<<g.num_sms, kHotWarps * 32, bytes, g.stream>>>(ea, nhot);
+        GGB_CUDA(cudaGetLastError());
+    }
+
     template <int MODE>
     static void launch_edge(DevGraph& g, const EdgeArgs<P, W>& ea) {
         edge_kernel<P, W, MODE><<<grid_edge<MODE>(g), kBlockThreads, 0, g.stream>>>(ea);
@@ -221,6 +249,10 @@ struct Engine {
         const bool msgs_fit_l2 = (uint64_t)n * sizeof(Msg) <= (64ull << 20);
         const uint32_t hot_limit = (g.nranks == 1 && !msgs_fit_l2)
             ? (uint32_t)std::min<uint64_t>(n, hot_bytes() / sizeof(Msg)) : 0u;
+        // hot slots copied into shared memory by the approximate gather (one
+        // rank: slot order = global heat order)
+        const uint32_t nhot = (kHotOK && g.nranks == 1)
+            ? (uint32_t)std::min<uint64_t>(n, smem_hot_bytes() / sizeof(Msg)) : 0u;
         const uint32_t l2_limit =
             g.nranks == 1 ? (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg)) : 0u;
 
@@ -291,6 +323,9 @@ struct Engine {
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
                 if (super && stash) launch_edge<kEdgeFoldStash>(g, ea);
                 else if (super) launch_edge<kEdgeSuper>(g, ea);
+                else if (all_proc && nhot) {
+                    if constexpr (kHotOK) launch_edge_hot(g, ea, nhot);
+                }
                 else if (all_proc) launch_edge<kEdgePlain>(g, ea);
                 else launch_edge<kEdgeCheck>(g, ea);
                 ++launches;

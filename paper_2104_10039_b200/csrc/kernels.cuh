@@ -158,7 +158,9 @@ __device__ __forceinline__ void for_run(F&& f) {
 template <class P>
 __host__ __device__ constexpr int stash_row_bytes() {
     constexpr int b = (int)sizeof(typename P::Message) * kRun;
-    return (b % 16 == 0 && ((b / 16) & (b / 16 - 1)) == 0 && b <= 256) ? b : 0;
+    // static shared memory: 32 rows per warp within 32 KB per block
+    return (b % 16 == 0 && ((b / 16) & (b / 16 - 1)) == 0 && b * 32 * kWarpsPerBlock <= 32768) ? b
+                                                                                                : 0;
 }
 
 template <class W>
@@ -166,11 +168,18 @@ using WStore = std::conditional_t<std::is_void_v<W>, char, W>;
 
 // Load this lane's sources (aligned run -> 4 x 128-bit) and issue its
 // message gathers back to back.
-template <class P, class W>
+// Shared-memory copy of the hottest message slots (edge_kernel_hot).
+struct HotTable {
+    uint32_t base = 0;  // shared-space address of slot 0
+    uint32_t n = 0;     // slots [0, n) are in shared memory
+};
+
+template <class P, class W, bool HOT = false>
 __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, uint64_t lo,
                                          uint64_t hi, typename P::Message (&m)[kRun],
                                          WStore<W> (&wr)[kRun], uint64_t pol_stream,
-                                         uint64_t pol_hot, uint64_t pol_cold) {
+                                         uint64_t pol_hot, uint64_t pol_cold,
+                                         HotTable ht = {}) {
     uint32_t s[kRun];
     if (lo == P0 && hi == P0 + kRun) {
         const uint4* sp = reinterpret_cast<const uint4*>(a.src + P0);
@@ -194,7 +203,10 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
     // inside the padded allocation.
 #pragma unroll
     for (int j = 0; j < kRun; ++j) {
-        if constexpr (fold_unroll<P>() != 1)
+        if constexpr (HOT)
+            m[j] = ld_msg_hot(a.msg_cur + s[j], ht.base + s[j] * (uint32_t)sizeof(typename P::Message),
+                              s[j] < ht.n ? 0u : (s[j] < a.hot_limit ? 1u : 2u), pol_hot, pol_cold);
+        else if constexpr (fold_unroll<P>() != 1)
             m[j] = ld_msg2(a.msg_cur + s[j], s[j] < a.hot_limit, pol_hot, pol_cold);
         else
             m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.l2_limit ? pol_hot : pol_cold);
@@ -225,10 +237,10 @@ __device__ __forceinline__ void write_flags(uint32_t* __restrict__ bitmap, uint6
     }
 }
 
-template <class P, class W, int MODE, bool PASS2>
+template <class P, class W, int MODE, bool PASS2, bool HOT = false>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, char* xs,
                                           uint64_t t, int lane, uint64_t pol_stream,
-                                          uint64_t pol_hot, uint64_t pol_cold) {
+                                          uint64_t pol_hot, uint64_t pol_cold, HotTable ht = {}) {
     using Accum = typename P::Accum;
     using Message = typename P::Message;
     constexpr bool SUPER = MODE == kEdgeSuper;
@@ -252,7 +264,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
             ri = a.run_i[r];
-            load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
+            load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
     uint32_t cnt = 2;  // pass 2 only needs the first vertex's start and end
@@ -276,7 +288,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
             ri = a.run_i[r];
-            load_run(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold);
+            load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
     const int rlo = (int)(lo - tstart), rhi = (int)(hi - tstart);  // task-relative
@@ -420,6 +432,34 @@ edge_kernel(const EdgeArgs<P, W> a) {
         edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], xs_all[threadIdx.x >> 5], t,
                                      lane, pol_stream, pol_hot, pol_cold);
     }
+}
+
+// The approximate gather with the hottest message slots copied into shared
+// memory: one 24-warp CTA per SM; gathers of slots < nhot are LDS (no L1 tag
+// or L2 request), the rest go to global memory as in edge_kernel. Every
+// result is identical to edge_kernel's (the table is a copy of msg_cur).
+constexpr int kHotWarps = 24;
+template <class P, class W, int MODE>
+__global__ void __launch_bounds__(kHotWarps * 32, 1)
+edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
+    using Message = typename P::Message;
+    extern __shared__ __align__(16) unsigned char hot_raw[];
+    __shared__ int16_t st_all[kHotWarps][kStageStarts];
+    Message* hot = reinterpret_cast<Message*>(hot_raw);
+    for (uint32_t i = threadIdx.x; i < nhot; i += blockDim.x) hot[i] = a.msg_cur[i];
+    __syncthreads();
+    HotTable ht;
+    ht.base = smem_u32(hot);
+    ht.n = nhot;
+    const int lane = threadIdx.x & 31;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_hot = policy_evict_last();
+    const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
+    const uint64_t warps = (uint64_t)gridDim.x * kHotWarps;
+    for (uint64_t t = (uint64_t)blockIdx.x * kHotWarps + (threadIdx.x >> 5); t < a.ntasks;
+         t += warps)
+        edge_task<P, W, MODE, false, true>(a, st_all[threadIdx.x >> 5], nullptr, t, lane,
+                                           pol_stream, pol_hot, pol_cold, ht);
 }
 
 template <class P, class W>
