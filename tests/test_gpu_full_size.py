@@ -1,0 +1,95 @@
+"""Parity at the BASELINE configs' FULL sizes (c2-c5): the device engine
+against the unmodified reference gg::run (oracle/_ref, all host threads) on
+the same R-MAT graph, generated on the device and exported.
+
+Per config: identical iteration count, per-iteration mode / processed_edges
+/ active_vertices (after a superstep these counts pin the kept-edge masks),
+and final properties bit-exact (SSSP u32 distances, WCC labels) or within
+the stated relative tolerance (PR 1e-9, fp32-stored BP 2e-6).
+Iteration budgets are capped so every reference run stays within tens of
+seconds; each cap still covers the first superstep (t = alpha + 1 = 5) and
+the approximate iterations on both sides of it.
+
+c2 also checks that the device R-MAT generator reproduces the CPU
+generator (oracle/gg_oracle.c, og_rmat) at full scale.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import GG, Oracle, Reference
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+THREADS = os.cpu_count() or 1
+RTOL = {"pr": 1e-9, "bp": 2e-6}
+
+
+def _run_both(ggb, name, max_iterations):
+    import bench
+    wl = bench.WORKLOADS[name]
+    dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],
+                              weights=wl["weights"])
+    program = bench.make_program(ggb, wl, dg, dg.n)
+    cfg = ggb.EngineConfig("gg", bench.SIGMA, wl["theta"], bench.ALPHA, max_iterations,
+                           wl["seed"])
+    rep = ggb.run(dg, program, cfg)
+    host = dg.to_host()
+    dg.close()
+    g = bench.ref_inputs(wl, host)
+    prog, pp = bench.ref_params(wl, g)
+    ref = Reference.run(g, prog, scheme=GG, sigma=bench.SIGMA, theta=wl["theta"],
+                        alpha=bench.ALPHA, max_iterations=max_iterations, seed=wl["seed"],
+                        threads=THREADS, **pp)
+    assert ref.status == 0, ref.msg
+    return wl, rep, ref, host
+
+
+def _check_records(rep, ref):
+    assert rep.iterations_run == ref.iterations_run
+    assert [int(r.mode) for r in rep.per_iteration] == ref.modes
+    assert [r.processed_edges for r in rep.per_iteration] == ref.processed_edges
+    assert [r.active_vertices for r in rep.per_iteration] == ref.active_vertices
+    assert 2 in ref.modes, "the capped budget must include a superstep"
+
+
+@pytest.fixture(scope="module")
+def need_reference():
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libggref.so not built")
+
+
+def test_c2_sssp_full_scale(ggb, need_reference):
+    wl, rep, ref, host = _run_both(ggb, "c2", 12)
+    _check_records(rep, ref)
+    d = np.asarray(rep.final_properties)
+    assert np.array_equal(d, ref.props)  # u32 distances, exact
+    # the device generator equals the CPU generator at full scale
+    cpu = Oracle.rmat(wl["scale"], wl["ef"], wl["seed"], threads=THREADS)
+    assert np.array_equal(cpu.off, host.in_offsets)
+    assert np.array_equal(cpu.src, host.in_sources)
+    w = Oracle.rmat_weights_u32(cpu.e, wl["seed"])
+    assert np.array_equal(w, host.weights)
+
+
+def test_c3_wcc_full_scale(ggb, need_reference):
+    _, rep, ref, _ = _run_both(ggb, "c3", 8)
+    _check_records(rep, ref)
+    assert np.array_equal(np.asarray(rep.final_properties), ref.props)
+
+
+def test_c4_bp_full_scale(ggb, need_reference):
+    _, rep, ref, _ = _run_both(ggb, "c4", 6)
+    _check_records(rep, ref)
+    np.testing.assert_allclose(np.asarray(rep.final_properties).reshape(-1),
+                               np.asarray(ref.props).reshape(-1), rtol=RTOL["bp"], atol=0)
+
+
+def test_c5_pagerank_full_scale(ggb, need_reference):
+    _, rep, ref, _ = _run_both(ggb, "c5", 6)
+    _check_records(rep, ref)
+    np.testing.assert_allclose(np.asarray(rep.final_properties), ref.props, rtol=RTOL["pr"],
+                               atol=0)
