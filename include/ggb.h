@@ -195,6 +195,12 @@ gg_status gg_partition_plan(uint64_t n, const uint64_t* offsets, int nranks, uin
 gg_status gg_nccl_unique_id(uint8_t out[128]);
 gg_status gg_exchange_nccl_create(const uint8_t unique_id[128], int rank, int nranks,
                                   gg_exchange** out, gg_error* err);
+/* In-process transport: nranks handles (out[nranks]) for ranks that are host
+ * threads of ONE process, each with its own graph and stream, on any devices
+ * (one GPU may host them all). Same engine code path as NCCL; collectives are
+ * host barriers + device copies. For single-GPU validation of the partitioned
+ * engine and for multi-tenant hosts. Destroy each handle. */
+gg_status gg_exchange_local_group(int nranks, gg_exchange** out);
 gg_status gg_exchange_destroy(gg_exchange* x);
 
 /* Host metrics (metrics.cpp:60-113); accuracy = (1 - err) * 100. */

@@ -1,7 +1,10 @@
 // exchange.cu — NCCL transport for the partitioned engine (see exchange.cuh).
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <mutex>
+#include <vector>
 
 #include "exchange.cuh"
 #include "kernels.cuh"
@@ -36,6 +39,50 @@ const NcclApi& nccl() {
     return api;
 }
 
+// In-process transport: the ranks are host threads of one process, each
+// with its own DevGraph and stream (any devices, including one shared
+// device). Collectives are host barriers plus device-to-device copies; no
+// kernel ever waits on another rank's kernel. It runs the partitioned engine
+// end to end where only one GPU is available (tests/test_gpu_multirank.py);
+// the NCCL transport carries the same calls across processes and GPUs.
+struct LocalGroup {
+    explicit LocalGroup(int n) : nranks(n), bufs(n), vals(n), ctrs(n) {}
+    int nranks;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t phase = 0;
+    std::vector<void*> bufs;
+    std::vector<uint64_t> vals;
+    std::vector<IterCounters> ctrs;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t my = phase;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++phase;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return phase != my; });
+        }
+    }
+};
+
+static void local_slices(DevGraph& g, LocalGroup& L, void* buf, size_t elem) {
+    GGB_CUDA(cudaStreamSynchronize(g.stream));  // this rank's slice is written
+    L.bufs[g.rank] = buf;
+    L.barrier();
+    for (int r = 0; r < g.nranks; ++r) {
+        const uint64_t b = g.bounds[r], e = g.bounds[r + 1];
+        if (r == g.rank || e == b) continue;
+        GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(buf) + b * elem,
+                                 static_cast<const char*>(L.bufs[r]) + b * elem, (e - b) * elem,
+                                 cudaMemcpyDefault, g.stream));
+    }
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    L.barrier();  // nobody rewrites its buffer while another rank copies from it
+}
+
 static void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) {
         const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
@@ -45,6 +92,7 @@ static void nccl_check(ncclResult_t r, const char* what) {
 
 void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size) {
     if (g.nranks <= 1) return;
+    if (g.exchange && g.exchange->local) return local_slices(g, *g.exchange->local, global_buf, elem_size);
     if (!g.exchange || !g.exchange->comm) throw Error(GG_NCCL, "multi-rank graph without exchange");
     const NcclApi& api = nccl();
     nccl_check(api.GroupStart(), "ncclGroupStart");
@@ -60,6 +108,15 @@ void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size) {
 
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
     if (g.nranks <= 1) return 0;
+    if (g.exchange && g.exchange->local) {
+        LocalGroup& L = *g.exchange->local;
+        L.vals[g.rank] = local;
+        L.barrier();
+        uint64_t base = 0;
+        for (int r = 0; r < g.rank; ++r) base += L.vals[r];
+        L.barrier();
+        return base;
+    }
     const NcclApi& api = nccl();
     uint64_t* d = g.ws.get<uint64_t>("xbase", (uint64_t)g.nranks + 1);
     GGB_CUDA(cudaMemcpyAsync(d + g.rank, &local, 8, cudaMemcpyHostToDevice, g.stream));
@@ -78,6 +135,27 @@ uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
 
 void exchange_counters(DevGraph& g, void* ctr_v) {
     if (g.nranks <= 1) return;
+    if (g.exchange && g.exchange->local) {
+        LocalGroup& L = *g.exchange->local;
+        IterCounters* d = static_cast<IterCounters*>(ctr_v);
+        GGB_CUDA(cudaMemcpyAsync(&L.ctrs[g.rank], d, sizeof(IterCounters), cudaMemcpyDeviceToHost,
+                                 g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        L.barrier();
+        IterCounters s{};
+        s.bad_min = 0xffffffffu;
+        for (const IterCounters& c : L.ctrs) {  // same reductions as the NCCL path
+            s.gathered += c.gathered;
+            s.processed += c.processed;
+            s.changed += c.changed;
+            s.any_invalid += c.any_invalid;
+            s.bad_min = std::min(s.bad_min, c.bad_min);
+        }
+        L.barrier();
+        GGB_CUDA(cudaMemcpyAsync(d, &s, sizeof(IterCounters), cudaMemcpyHostToDevice, g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));  // `s` is a stack variable
+        return;
+    }
     const NcclApi& api = nccl();
     IterCounters* ctr = static_cast<IterCounters*>(ctr_v);
     nccl_check(api.GroupStart(), "ncclGroupStart");
@@ -119,6 +197,20 @@ gg_status gg_exchange_nccl_create(const uint8_t unique_id[128], int rank, int nr
             ggb::nccl_check(r, "ncclCommInitRank");
         }
         *out = x;
+    });
+}
+
+gg_status gg_exchange_local_group(int nranks, gg_exchange** out) {
+    return ggb::guarded(nullptr, [&] {
+        if (nranks < 1) throw ggb::Error(GG_INVALID_ARGUMENT, "nranks must be >= 1");
+        auto grp = std::make_shared<ggb::LocalGroup>(nranks);
+        for (int r = 0; r < nranks; ++r) {
+            auto* x = new gg_exchange;
+            x->rank = r;
+            x->nranks = nranks;
+            x->local = grp;
+            out[r] = x;
+        }
     });
 }
 

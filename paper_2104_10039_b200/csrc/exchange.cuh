@@ -9,11 +9,18 @@
 
 #include <nccl.h>
 
+#include <memory>
+
 #include "graph.cuh"
+
+namespace ggb {
+struct LocalGroup;  // in-process transport (exchange.cu)
+}
 
 struct gg_exchange {
     int rank = 0, nranks = 1;
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;               // NCCL transport (one process per GPU)
+    std::shared_ptr<ggb::LocalGroup> local;  // or: ranks as threads of one process
 };
 
 namespace ggb {

@@ -469,6 +469,20 @@ class Exchange:
         self.handle = h
         self.rank, self.nranks = rank, nranks
 
+    @classmethod
+    def local_group(cls, nranks: int) -> list["Exchange"]:
+        """In-process transport: one handle per rank for ranks run as threads of
+        this process (each with its own DeviceGraph; one GPU may host all)."""
+        hs = (C.c_void_p * nranks)()
+        _raise(L.lib().gg_exchange_local_group(nranks, hs), None)
+        out = []
+        for r in range(nranks):
+            x = cls.__new__(cls)
+            x.handle = C.c_void_p(hs[r])
+            x.rank, x.nranks = r, nranks
+            out.append(x)
+        return out
+
     @staticmethod
     def unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()

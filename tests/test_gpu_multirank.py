@@ -1,0 +1,110 @@
+"""The partitioned (multi-rank) engine on real device code, one GPU.
+
+Ranks run as host threads of this process, each with its own DeviceGraph
+slice and stream, joined by the in-process transport
+(gg_exchange_local_group): the same engine code path the NCCL transport
+drives across GPUs (partition plan, offset rebase, global-position padding of
+each rank's lists, per-iteration slice exchange and counter reduction, the
+sparsified list's global base) with host barriers and device copies standing
+in for the collectives. No kernel waits on another rank's kernel.
+
+The bar is the analogue of test_engine.cpp:161-182: properties and
+per-iteration records bit-identical to the single-rank run, for every
+program and scheme.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(ggb, scale, ef, seed, sym=False, weights=None):
+    g = Oracle.rmat(scale, ef, seed)
+    if sym:
+        g = Oracle.symmetrized(g)
+    w = None
+    if weights == "u32":
+        w = Oracle.rmat_weights_u32(g.e, seed)
+    elif weights == "coupling":
+        w = Oracle.bp_couplings(g.e, seed)
+    return ggb.Graph(g.n, g.off, g.src, w, g.outdeg)
+
+
+def _program(ggb, prog, graph, seed):
+    if prog == "pr":
+        return ggb.pagerank_spec(0.85, 1e-7)
+    if prog == "sssp":
+        return ggb.sssp_spec(int(np.argmax(graph.out_degree)), True)
+    if prog == "wcc":
+        return ggb.wcc_spec()
+    return ggb.EdgeBeliefPropagationProgram(ggb.bp_priors(graph.n, seed), 1e-6)
+
+
+def _run_ranks(ggb, graph, program, cfg, nranks):
+    xs = ggb.Exchange.local_group(nranks)
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            dg = ggb.DeviceGraph.upload(graph, device=0, rank=r, nranks=nranks,
+                                        exchange=xs[r].handle)
+            out[r] = ggb.run(dg, program, cfg)
+            dg.close()
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    for x in xs:
+        x.close()
+    assert not errs, errs
+    return out
+
+
+def _same(a, b):
+    assert a.iterations_run == b.iterations_run
+    assert [int(r.mode) for r in a.per_iteration] == [int(r.mode) for r in b.per_iteration]
+    assert [r.processed_edges for r in a.per_iteration] == [r.processed_edges for r in b.per_iteration]
+    assert [r.active_vertices for r in a.per_iteration] == [r.active_vertices for r in b.per_iteration]
+    pa, pb = np.asarray(a.final_properties), np.asarray(b.final_properties)
+    assert pa.shape == pb.shape
+    assert np.array_equal(pa.view(np.uint8), pb.view(np.uint8)), "not bit-identical"
+
+
+CASES = [  # prog, scale, edge factor, seed, symmetrise, weights, theta
+    ("pr", 15, 16, 3, False, None, 0.01),
+    ("sssp", 15, 16, 4, False, "u32", 0.05),
+    ("wcc", 14, 16, 5, True, None, 0.0),
+    ("bp", 14, 16, 6, False, "coupling", 0.01),
+]
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_ranks_bit_identical_to_one_gpu(ggb, case, nranks):
+    prog, scale, ef, seed, sym, weights, theta = case
+    graph = _graph(ggb, scale, ef, seed, sym, weights)
+    program = _program(ggb, prog, graph, seed)
+    cfg = ggb.EngineConfig("gg", 0.5, theta, 2, 30, seed)
+    single = ggb.run(graph, program, cfg)
+    for rep in _run_ranks(ggb, graph, program, cfg, nranks):
+        _same(rep, single)
+
+
+@pytest.mark.parametrize("scheme", ["accurate", "sp", "sms", "gg"])
+def test_ranks_all_schemes_pagerank(ggb, scheme):
+    graph = _graph(ggb, 16, 16, 7)
+    program = ggb.pagerank_spec(0.85, 1e-7)
+    cfg = ggb.EngineConfig(scheme, 0.5, 0.01, 3, 25, 7)
+    single = ggb.run(graph, program, cfg)
+    for rep in _run_ranks(ggb, graph, program, cfg, 4):
+        _same(rep, single)
