@@ -290,7 +290,7 @@ __global__ void relabel_kernel(uint32_t* __restrict__ src, uint64_t count,
         src[i] = __ldg(slot_of + src[i]);
 }
 
-void assign_slots(DevGraph& g) {
+void compute_slots(DevGraph& g) {
     const uint64_t n = g.n;
     g.slot_of = static_cast<decltype(g.slot_of)>(dev_alloc((n + 1) * 4, g.stream));
     g.vtx_of_slot = static_cast<decltype(g.vtx_of_slot)>(dev_alloc((n + 1) * 4, g.stream));
@@ -317,13 +317,19 @@ void assign_slots(DevGraph& g) {
                                              g.stream));
     slot_fill_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(v1, n, g.slot_of, g.vtx_of_slot);
     GGB_CUDA(cudaGetLastError());
-    if (g.e_loc) {
-        relabel_kernel<<<grid_for(g.e_loc, 256), 256, 0, g.stream>>>(g.src + g.full.pad, g.e_loc,
-                                                                      g.slot_of);
-        GGB_CUDA(cudaGetLastError());
-    }
-    GGB_CUDA(cudaStreamSynchronize(g.stream));
     dev_free(k0, g.stream); dev_free(k1, g.stream); dev_free(v0, g.stream); dev_free(v1, g.stream); dev_free(db, g.stream); dev_free(tmpp, g.stream);
+}
+
+void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count) {
+    if (!count) return;
+    relabel_kernel<<<grid_for(count, 256), 256, 0, g.stream>>>(src, count, g.slot_of);
+    GGB_CUDA(cudaGetLastError());
+}
+
+void assign_slots(DevGraph& g) {
+    compute_slots(g);
+    relabel_sources(g, g.src + g.full.pad, g.e_loc);
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
 }
 
 __global__ void unlabel_kernel(const uint32_t* __restrict__ src, uint64_t count,

@@ -43,11 +43,15 @@ static void setup_common(DevGraph& g, const gg_part_opts* opts) {
     if (count < 1) throw Error(GG_CUDA, "no CUDA device");
     g.device = dev;
     GGB_CUDA(cudaSetDevice(dev));
-    cudaDeviceProp prop;
-    GGB_CUDA(cudaGetDeviceProperties(&prop, dev));
-    if (prop.major < 10)
+    int major = 0, sms = 0;  // attribute queries: cheap on the e2e path
+    GGB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    GGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (major < 10) {
+        cudaDeviceProp prop;
+        GGB_CUDA(cudaGetDeviceProperties(&prop, dev));
         throw Error(GG_CUDA, std::string("libggb.so needs an sm_100 device, found ") + prop.name);
-    g.num_sms = prop.multiProcessorCount;
+    }
+    g.num_sms = sms;
     GGB_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
     g.ws.stream = g.stream;
     // keep freed device memory cached in the stream-ordered pool (graphs are
@@ -105,6 +109,28 @@ gg_status gg_partition_plan(uint64_t n, const uint64_t* offsets, int nranks, uin
     });
 }
 
+// Copy stream + events of one pipelined upload (released on every exit path).
+constexpr size_t kUploadChunks = 16;
+struct Upload {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready = nullptr, deg = nullptr, off = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> chunk;
+    Upload(cudaStream_t, size_t nchunks) : chunk(nchunks, nullptr) {
+        GGB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&ready, &deg, &off, &done})
+            GGB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        for (cudaEvent_t& e : chunk) GGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    ~Upload() {
+        if (cs) cudaStreamSynchronize(cs);
+        for (cudaEvent_t e : {ready, deg, off, done})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : chunk)
+            if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamDestroy(cs);
+    }
+};
+
 gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                               gg_dev_graph** out, gg_error* err) {
     return guarded(err, [&] {
@@ -128,43 +154,59 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
             g.off = static_cast<decltype(g.off)>(dev_alloc((g.nloc + 1) * 8, g.stream));
             g.src = static_cast<decltype(g.src)>(dev_alloc((pad + g.e_loc + kRun) * 4, g.stream));
             g.outdeg = static_cast<decltype(g.outdeg)>(dev_alloc((g.n + 1) * 4, g.stream));
-            // the owned offsets straight from the caller's buffer, rebased on device
+            const size_t wb = weight_size(g.wkind);
+            if (wb) g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
+            g.full.pad = pad;
+            std::vector<uint32_t> host_deg;
+            if (!csc->out_degree) {  // reference graphs carry it; compute for bare CSC views
+                host_deg.assign(g.n, 0);
+                for (uint64_t i = 0; i < csc->e; ++i) {
+                    if (csc->sources[i] >= g.n)
+                        throw Error(GG_INVALID_ARGUMENT, "edge source out of range");
+                    ++host_deg[csc->sources[i]];
+                }
+            }
+            const uint32_t* deg = csc->out_degree ? csc->out_degree : host_deg.data();
+            // Pipelined upload: the copy stream carries out-degrees, offsets,
+            // then the sources in chunks and the weights over PCIe while the
+            // graph stream computes the slot order, the run map and relabels
+            // each source chunk as it lands.
+            Upload up(g.stream, g.e_loc ? kUploadChunks : 0);
+            GGB_CUDA(cudaEventRecord(up.ready, g.stream));  // allocations above
+            GGB_CUDA(cudaStreamWaitEvent(up.cs, up.ready, 0));
+            if (g.n) GGB_CUDA(cudaMemcpyAsync(g.outdeg, deg, g.n * 4, cudaMemcpyHostToDevice, up.cs));
+            GGB_CUDA(cudaEventRecord(up.deg, up.cs));
             GGB_CUDA(cudaMemcpyAsync(g.off, csc->offsets ? csc->offsets + g.v_begin : &zero,
-                                     (g.nloc + 1) * 8, cudaMemcpyHostToDevice, g.stream));
+                                     (g.nloc + 1) * 8, cudaMemcpyHostToDevice, up.cs));
+            GGB_CUDA(cudaEventRecord(up.off, up.cs));
+            const uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
+            for (size_t k = 0; k < up.chunk.size(); ++k) {
+                const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
+                if (e > b)
+                    GGB_CUDA(cudaMemcpyAsync(g.src + pad + b, csc->sources + g.e_base + b, (e - b) * 4,
+                                             cudaMemcpyHostToDevice, up.cs));
+                GGB_CUDA(cudaEventRecord(up.chunk[k], up.cs));
+            }
+            if (wb && g.e_loc)
+                GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
+                                         static_cast<const char*>(csc->weights) + g.e_base * wb,
+                                         g.e_loc * wb, cudaMemcpyHostToDevice, up.cs));
+            GGB_CUDA(cudaEventRecord(up.done, up.cs));
+            // graph stream
+            GGB_CUDA(cudaStreamWaitEvent(g.stream, up.deg, 0));
+            compute_slots(g);
+            GGB_CUDA(cudaStreamWaitEvent(g.stream, up.off, 0));
             if (g.e_base) {
                 rebase_kernel<<<256, 256, 0, g.stream>>>(g.off, g.nloc + 1, g.e_base, g.off);
                 GGB_CUDA(cudaGetLastError());
             }
-            if (g.e_loc)
-                GGB_CUDA(cudaMemcpyAsync(g.src + pad, csc->sources + g.e_base, g.e_loc * 4,
-                                         cudaMemcpyHostToDevice, g.stream));
-            const size_t wb = weight_size(g.wkind);
-            if (wb) {
-                g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
-                if (g.e_loc)
-                    GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
-                                             static_cast<const char*>(csc->weights) + g.e_base * wb,
-                                             g.e_loc * wb, cudaMemcpyHostToDevice, g.stream));
-            }
-            g.full.pad = pad;
-            if (csc->out_degree) {
-                if (g.n)
-                    GGB_CUDA(cudaMemcpyAsync(g.outdeg, csc->out_degree, g.n * 4,
-                                             cudaMemcpyHostToDevice, g.stream));
-            } else {
-                std::vector<uint32_t> deg(g.n, 0);
-                for (uint64_t i = 0; i < csc->e; ++i) {
-                    if (csc->sources[i] >= g.n)
-                        throw Error(GG_INVALID_ARGUMENT, "edge source out of range");
-                    ++deg[csc->sources[i]];
-                }
-                if (g.n)
-                    GGB_CUDA(cudaMemcpyAsync(g.outdeg, deg.data(), g.n * 4, cudaMemcpyHostToDevice,
-                                             g.stream));
-                GGB_CUDA(cudaStreamSynchronize(g.stream));
-            }
-            assign_slots(g);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
+            for (size_t k = 0; k < up.chunk.size(); ++k) {
+                const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
+                GGB_CUDA(cudaStreamWaitEvent(g.stream, up.chunk[k], 0));
+                relabel_sources(g, g.src + pad + b, e - b);
+            }
+            GGB_CUDA(cudaStreamWaitEvent(g.stream, up.done, 0));
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
             delete h;

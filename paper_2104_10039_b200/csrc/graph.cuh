@@ -137,6 +137,10 @@ void bp_priors_device(uint64_t n, uint64_t seed, float* out, cudaStream_t st);
 // Hot-first message slots (slot_of / vtx_of_slot) and the rewrite of the
 // full list's sources from vertex ids to slot ids.
 void assign_slots(DevGraph& g);
+// the two halves of assign_slots, for the pipelined upload: slot_of /
+// vtx_of_slot (stream-ordered, no sync) and the in-place source relabel
+void compute_slots(DevGraph& g);
+void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count);
 // Copy the full list's sources back to host as vertex ids.
 void export_sources(const DevGraph& g, uint32_t* host_out);
 // Size `meta` for (pad, e) and build its run -> vertex map from `off`.
