@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GGB_ABI_VERSION 2
+#define GGB_ABI_VERSION 3
 
 typedef enum gg_status {
     GG_OK = 0,
@@ -129,6 +129,7 @@ typedef struct gg_bp_params {                                                   
      * table (float[n*2]), the coupling from each edge's weight, and beliefs
      * are stored as fp32 (states must be 2). */
     const float* prior_table;
+    int32_t prior_on_device;    /* 1: prior_table is device memory (no per-run copy) */
 } gg_bp_params;
 
 const char* gg_status_string(gg_status s);
@@ -159,6 +160,12 @@ gg_status gg_dev_graph_export(const gg_dev_graph* g, uint64_t* offsets, uint32_t
                               void* weights, uint32_t* out_degree);
 /* BASELINE C4 priors generated on device (float[2n]); copied to host if out != NULL. */
 gg_status gg_bp_priors(uint64_t n, uint64_t seed, float* out);
+/* ... or left in device memory (*dev_out, free with gg_device_free). */
+gg_status gg_bp_priors_device(uint64_t n, uint64_t seed, float** dev_out);
+/* Device copy of a host buffer (e.g. a caller's prior table kept resident
+ * across runs); free with gg_device_free. */
+gg_status gg_device_upload(const void* host, uint64_t bytes, void** dev_out);
+gg_status gg_device_free(void* dev);
 
 /* Runs (engine.hpp:141-249). out_props: host buffer of n * prop_size
  * (pr/sssp: double; wcc: uint32; bp: double[states]). recs: rec_cap

@@ -8,7 +8,7 @@ from ._lib import lib as _load
 _load()
 
 from .engine import (  # noqa: E402
-    Exchange, bp_priors,
+    DeviceBuffer, Exchange, bp_priors,
     BeliefPropagationProgram, DeviceGraph, EdgeBeliefPropagationProgram, EngineConfig, EngineError,
     ErrorReport, GgbError, Graph, IterationMode, IterationRecord, PageRankProgram, RunReport,
     Scheme, SsspProgram, WccProgram, bp_spec, mode_for, pagerank_spec, partition_plan,
@@ -17,7 +17,7 @@ from .engine import (  # noqa: E402
 )
 
 __all__ = [
-    "Exchange", "bp_priors", "BeliefPropagationProgram", "DeviceGraph", "EdgeBeliefPropagationProgram", "EngineConfig",
+    "DeviceBuffer", "Exchange", "bp_priors", "BeliefPropagationProgram", "DeviceGraph", "EdgeBeliefPropagationProgram", "EngineConfig",
     "EngineError", "ErrorReport", "GgbError", "Graph", "IterationMode", "IterationRecord",
     "PageRankProgram", "RunReport", "Scheme", "SsspProgram", "WccProgram", "bp_spec", "mode_for",
     "pagerank_spec", "partition_plan", "relative_error", "run", "scheme_from_name",

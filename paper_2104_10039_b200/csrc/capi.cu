@@ -323,6 +323,33 @@ gg_status gg_bp_priors(uint64_t n, uint64_t seed, float* out) {
     });
 }
 
+gg_status gg_bp_priors_device(uint64_t n, uint64_t seed, float** dev_out) {
+    return guarded(nullptr, [&] {
+        if (!dev_out) throw Error(GG_INVALID_ARGUMENT, "null argument");
+        float* d = nullptr;
+        GGB_CUDA(cudaMalloc(&d, (2 * n + 2) * 4));
+        bp_priors_device(n, seed, d, 0);
+        GGB_CUDA(cudaStreamSynchronize(0));
+        *dev_out = d;
+    });
+}
+
+gg_status gg_device_upload(const void* host, uint64_t bytes, void** dev_out) {
+    return guarded(nullptr, [&] {
+        if (!dev_out || (bytes && !host)) throw Error(GG_INVALID_ARGUMENT, "null argument");
+        void* d = nullptr;
+        GGB_CUDA(cudaMalloc(&d, bytes ? bytes : 16));
+        if (bytes) GGB_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+        *dev_out = d;
+    });
+}
+
+gg_status gg_device_free(void* dev) {
+    return guarded(nullptr, [&] {
+        if (dev) GGB_CUDA(cudaFree(dev));
+    });
+}
+
 gg_status gg_validate(const gg_engine_config* cfg, gg_error* err) {
     return guarded(err, [&] { validate(*cfg); });
 }
@@ -440,8 +467,12 @@ gg_status gg_run_bp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_bp_pa
                 throw Error(GG_INVALID_ARGUMENT, "bp with a prior table needs per-edge couplings (f32/f64 weights)");
             RunIO io = make_io(cfg, recs, cap, sum, opts, out_props, 2);
             if (g.n == 0) return;
-            float2* table = g.ws.get<float2>("bp.prior", g.n);
-            GGB_CUDA(cudaMemcpyAsync(table, p->prior_table, g.n * 8, cudaMemcpyHostToDevice, g.stream));
+            const float2* table = reinterpret_cast<const float2*>(p->prior_table);
+            if (!p->prior_on_device) {  // host table: one copy per run
+                float2* d = g.ws.get<float2>("bp.prior", g.n);
+                GGB_CUDA(cudaMemcpyAsync(d, p->prior_table, g.n * 8, cudaMemcpyHostToDevice, g.stream));
+                table = d;
+            }
             BeliefPropEdge prog;
             prog.prior_table = table;
             prog.epsilon = p->epsilon;

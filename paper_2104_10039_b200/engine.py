@@ -215,8 +215,9 @@ class BeliefPropagationProgram:
 @dataclass(frozen=True)
 class EdgeBeliefPropagationProgram:
     """BASELINE C4: coupling per edge (the graph's weights), fp32 prior table
-    (float32[n, 2]), fp32 belief storage."""
-    priors: np.ndarray = field(default=None, repr=False, compare=False)
+    (float32[n, 2] on the host, copied every run, or a DeviceBuffer kept
+    resident), fp32 belief storage."""
+    priors: object = field(default=None, repr=False, compare=False)
     epsilon: float = 1e-6
 
 
@@ -379,15 +380,20 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
                                 C.byref(summ), C.byref(opts), C.byref(err))
         elif isinstance(program, BeliefPropagationProgram):
             props = _out_buffer(out, (n, program.states), np.float64)
-            p = L.BpParams(program.states, program.coupling, program.epsilon, None)
+            p = L.BpParams(program.states, program.coupling, program.epsilon, None, 0)
             rc = lib.gg_run_bp(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                C.byref(summ), C.byref(opts), C.byref(err))
         elif isinstance(program, EdgeBeliefPropagationProgram):
-            pri = np.ascontiguousarray(program.priors, np.float32).reshape(-1)
-            if pri.shape[0] != 2 * n:
-                raise ValueError("edge BP needs a float32[n, 2] prior table")
             props = _out_buffer(out, (n, 2), np.float64)
-            p = L.BpParams(2, 0.0, program.epsilon, pri.ctypes.data)
+            if isinstance(program.priors, DeviceBuffer):
+                if program.priors.nbytes < 8 * n:
+                    raise ValueError("edge BP needs a float32[n, 2] prior table")
+                p = L.BpParams(2, 0.0, program.epsilon, program.priors.ptr, 1)
+            else:
+                pri = np.ascontiguousarray(program.priors, np.float32).reshape(-1)
+                if pri.shape[0] != 2 * n:
+                    raise ValueError("edge BP needs a float32[n, 2] prior table")
+                p = L.BpParams(2, 0.0, program.epsilon, pri.ctypes.data, 0)
             rc = lib.gg_run_bp(dg._h, C.byref(ccfg), C.byref(p), props.ctypes.data, recs, cap,
                                C.byref(summ), C.byref(opts), C.byref(err))
         else:
@@ -495,8 +501,39 @@ class Exchange:
             self.handle = C.c_void_p()
 
 
-def bp_priors(n: int, seed: int) -> np.ndarray:
-    """BASELINE C4 priors generated on the device: float32[n, 2]."""
+class DeviceBuffer:
+    """Device memory owned by libggb (gg_device_upload / gg_bp_priors_device)."""
+
+    def __init__(self, ptr, nbytes: int):
+        self.ptr = ptr
+        self.nbytes = int(nbytes)
+
+    @classmethod
+    def upload(cls, array: np.ndarray) -> "DeviceBuffer":
+        a = np.ascontiguousarray(array)
+        h = C.c_void_p()
+        _raise(L.lib().gg_device_upload(a.ctypes.data, a.nbytes, C.byref(h)), None)
+        return cls(h, a.nbytes)
+
+    def close(self):
+        if self.ptr:
+            L.lib().gg_device_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def bp_priors(n: int, seed: int, device: bool = False):
+    """BASELINE C4 priors generated on the device: float32[n, 2] on the host,
+    or (device=True) a DeviceBuffer that stays resident."""
+    if device:
+        h = C.c_void_p()
+        _raise(L.lib().gg_bp_priors_device(n, seed, C.byref(h)), None)
+        return DeviceBuffer(h, 8 * n)
     out = np.zeros(2 * max(n, 1), np.float32)
     _raise(L.lib().gg_bp_priors(n, seed, out.ctypes.data), None)
     return out[:2 * n].reshape(n, 2)

@@ -168,6 +168,23 @@ def test_edge_bp_fp32(ggb, seed):
         assert mism == 0
 
 
+def test_edge_bp_resident_priors(ggb):
+    """A device-resident prior table (generated there, or uploaded once) gives
+    exactly the run a host table gives."""
+    n_seed = 3
+    dg = ggb.DeviceGraph.rmat(12, 16, n_seed, weights="coupling")
+    host = ggb.bp_priors(dg.n, n_seed)
+    assert np.array_equal(host, Oracle.bp_priors(dg.n, n_seed).reshape(dg.n, 2))
+    cfg = ggb.EngineConfig("gg", 0.5, 0.01, 4, 20, n_seed)
+    a = ggb.run(dg, ggb.EdgeBeliefPropagationProgram(host, 1e-6), cfg)
+    for pri in (ggb.bp_priors(dg.n, n_seed, device=True), ggb.DeviceBuffer.upload(host)):
+        b = ggb.run(dg, ggb.EdgeBeliefPropagationProgram(pri, 1e-6), cfg)
+        assert np.array_equal(a.final_properties, b.final_properties)
+        assert [r.processed_edges for r in a.per_iteration] == [r.processed_edges for r in b.per_iteration]
+        pri.close()
+    dg.close()
+
+
 def test_sssp_u32_weights_exact(ggb):
     g = Oracle.rmat(12, 16, 2)
     w = Oracle.rmat_weights_u32(g.e, 2)
