@@ -218,6 +218,23 @@ gg_status gg_relative_error(const double* approx, const double* exact, uint64_t 
 gg_status gg_stretch_error(const double* approx, const double* exact, uint64_t n,
                            double* err_out);
 
+/* The same metrics on DEVICE arrays (e.g. gg_last_projection of an exact and
+ * an approximate run): only the scalar returns to the host. top-k is exact;
+ * the two means are reduced in a fixed order (deterministic; equal to the
+ * reference's left-to-right sum up to rounding). stretch: a vertex with
+ * approx < exact returns GG_INVALID_ARGUMENT with err->vertex set. */
+gg_status gg_topk_error_dev(const double* approx, const double* exact, uint64_t n, uint64_t k,
+                            double* err_out);
+gg_status gg_relative_error_dev(const double* approx, const double* exact, uint64_t n,
+                                double* err_out);
+gg_status gg_stretch_error_dev(const double* approx, const double* exact, uint64_t n,
+                               double* err_out, gg_error* err);
+/* double[n] device projection of the graph's last run (PR rank, SSSP
+ * distance with +inf for unreached, WCC label, BP belief[0]); valid until the
+ * next run on this graph. Copy it (gg_device_copy) to keep it. */
+gg_status gg_last_projection(gg_dev_graph* g, const double** dev_out);
+gg_status gg_device_copy(const void* dev_src, uint64_t bytes, void** dev_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,7 +8,7 @@ from ._lib import lib as _load
 _load()
 
 from .engine import (  # noqa: E402
-    DeviceBuffer, Exchange, bp_priors,
+    DeviceBuffer, DeviceView, Exchange, bp_priors,
     BeliefPropagationProgram, DeviceGraph, EdgeBeliefPropagationProgram, EngineConfig, EngineError,
     ErrorReport, GgbError, Graph, IterationMode, IterationRecord, PageRankProgram, RunReport,
     Scheme, SsspProgram, WccProgram, bp_spec, mode_for, pagerank_spec, partition_plan,
@@ -17,7 +17,7 @@ from .engine import (  # noqa: E402
 )
 
 __all__ = [
-    "DeviceBuffer", "Exchange", "bp_priors", "BeliefPropagationProgram", "DeviceGraph", "EdgeBeliefPropagationProgram", "EngineConfig",
+    "DeviceBuffer", "DeviceView", "Exchange", "bp_priors", "BeliefPropagationProgram", "DeviceGraph", "EdgeBeliefPropagationProgram", "EngineConfig",
     "EngineError", "ErrorReport", "GgbError", "Graph", "IterationMode", "IterationRecord",
     "PageRankProgram", "RunReport", "Scheme", "SsspProgram", "WccProgram", "bp_spec", "mode_for",
     "pagerank_spec", "partition_plan", "relative_error", "run", "scheme_from_name",

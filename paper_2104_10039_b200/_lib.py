@@ -14,7 +14,8 @@ GG_W_NONE, GG_W_U32, GG_W_F32, GG_W_F64 = range(4)
 # every symbol include/ggb.h declares (checked at load and by tests)
 EXPORTS = (
     "gg_status_string", "gg_abi_version", "gg_bp_priors_device", "gg_device_upload",
-    "gg_device_free", "gg_dev_graph_create", "gg_dev_graph_destroy",
+    "gg_device_free", "gg_device_copy", "gg_last_projection", "gg_topk_error_dev",
+    "gg_relative_error_dev", "gg_stretch_error_dev", "gg_dev_graph_create", "gg_dev_graph_destroy",
     "gg_dev_graph_info", "gg_dev_graph_create_rmat", "gg_dev_graph_export", "gg_bp_priors",
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
@@ -114,6 +115,11 @@ def lib():
     L.gg_bp_priors_device.argtypes = [C.c_uint64, C.c_uint64, P(vp)]
     L.gg_device_upload.argtypes = [vp, C.c_uint64, P(vp)]
     L.gg_device_free.argtypes = [vp]
+    L.gg_device_copy.argtypes = [vp, C.c_uint64, P(vp)]
+    L.gg_last_projection.argtypes = [vp, P(vp)]
+    L.gg_topk_error_dev.argtypes = [vp, vp, C.c_uint64, C.c_uint64, P(C.c_double)]
+    L.gg_relative_error_dev.argtypes = [vp, vp, C.c_uint64, P(C.c_double)]
+    L.gg_stretch_error_dev.argtypes = [vp, vp, C.c_uint64, P(C.c_double), P(ErrorC)]
     L.gg_validate.argtypes = [P(EngineConfigC), P(ErrorC)]
     L.gg_mode_for.argtypes = [C.c_int32, C.c_uint64, C.c_uint64]
     L.gg_mode_for.restype = C.c_int32

@@ -412,6 +412,13 @@ struct Engine {
         GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
                                  cudaMemcpyDeviceToDevice, g.stream));
         if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
+        g.project_last = [&g, prog, final_all, n]() -> const double* {  // metrics.cu
+            double* proj = g.ws.get<double>("proj", n + 1);
+            export_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, final_all, n, 1, proj);
+            GGB_CUDA(cudaGetLastError());
+            GGB_CUDA(cudaStreamSynchronize(g.stream));
+            return proj;
+        };
         if (io.out_props && !(io.opts && io.opts->device_output)) {
             if constexpr (requires { P::kRawOutput; }) {  // WCC: uint32 labels as-is
                 GGB_CUDA(cudaMemcpyAsync(io.out_props, final_all, n * 4, cudaMemcpyDeviceToHost,

@@ -15,6 +15,7 @@
 // ListMeta, msg[2], prop, status[2], acc_out/hv/tv/carry, counters.
 #pragma once
 
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -108,6 +109,9 @@ struct DevGraph {
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     Workspace ws;
+    // double[n] projection of the last run's final properties, computed on
+    // demand in the workspace (valid until the next run); set by every run
+    std::function<const double*()> project_last;
     void* h_ctr = nullptr;            // pinned host mirror of the iteration counters
     cudaEvent_t ev[8] = {};           // timing events, created on first use
     void* host_counters(size_t bytes) {

@@ -131,6 +131,13 @@ class DeviceGraph:
                err)
         return cls(h, g.n, g.num_edges())
 
+    def last_projection(self) -> "DeviceView":
+        """double[n] device projection of the last run (PR rank, SSSP distance,
+        WCC label, BP belief[0]); valid until the next run on this graph."""
+        p = C.c_void_p()
+        _raise(L.lib().gg_last_projection(self._h, C.byref(p)), None)
+        return DeviceView(p, self.n)
+
     @classmethod
     def rmat(cls, scale, edge_factor, seed, a=0.57, b=0.19, c=0.19, symmetrize=False,
              weights=None, device=-1, rank=0, nranks=1, exchange=None):
@@ -429,6 +436,15 @@ class ErrorReport:
     k: int = 0
 
 
+def _on_device(*xs):
+    dev = [isinstance(x, (DeviceView, DeviceBuffer)) for x in xs]
+    if any(dev) and not all(dev):
+        raise TypeError("metric inputs must both be host arrays or both device arrays")
+    if all(dev) and xs[0].n != xs[1].n:
+        raise ValueError("metric inputs have different lengths")
+    return all(dev)
+
+
 def _metric_args(approx, exact):
     a = np.ascontiguousarray(approx, np.float64)
     x = np.ascontiguousarray(exact, np.float64)
@@ -438,22 +454,37 @@ def _metric_args(approx, exact):
 
 
 def topk_error(approx, exact, k: int) -> ErrorReport:
-    a, x = _metric_args(approx, exact)
+    """metrics.cpp:60-72; host arrays, or device arrays (DeviceView /
+    DeviceBuffer: computed on the GPU, only the scalar comes back)."""
     out = C.c_double()
+    if _on_device(approx, exact):
+        _raise(L.lib().gg_topk_error_dev(approx.ptr, exact.ptr, approx.n, int(k), C.byref(out)), None)
+        return ErrorReport("topk", out.value, (1.0 - out.value) * 100.0, int(k))
+    a, x = _metric_args(approx, exact)
     _raise(L.lib().gg_topk_error(a.ctypes.data, x.ctypes.data, len(a), int(k), C.byref(out)), None)
     return ErrorReport("topk", out.value, (1.0 - out.value) * 100.0, int(k))
 
 
 def relative_error(approx, exact) -> ErrorReport:
-    a, x = _metric_args(approx, exact)
     out = C.c_double()
+    if _on_device(approx, exact):
+        _raise(L.lib().gg_relative_error_dev(approx.ptr, exact.ptr, approx.n, C.byref(out)), None)
+        return ErrorReport("relative", out.value, (1.0 - out.value) * 100.0)
+    a, x = _metric_args(approx, exact)
     _raise(L.lib().gg_relative_error(a.ctypes.data, x.ctypes.data, len(a), C.byref(out)), None)
     return ErrorReport("relative", out.value, (1.0 - out.value) * 100.0)
 
 
 def stretch_error(approx, exact) -> ErrorReport:
-    a, x = _metric_args(approx, exact)
     out = C.c_double()
+    if _on_device(approx, exact):
+        err = L.ErrorC()
+        rc = L.lib().gg_stretch_error_dev(approx.ptr, exact.ptr, approx.n, C.byref(out), C.byref(err))
+        if rc == L.GG_INVALID_ARGUMENT:
+            raise RuntimeError(err.msg.decode())
+        _raise(rc, err)
+        return ErrorReport("stretch", out.value, (1.0 - out.value) * 100.0)
+    a, x = _metric_args(approx, exact)
     rc = L.lib().gg_stretch_error(a.ctypes.data, x.ctypes.data, len(a), C.byref(out))
     if rc == L.GG_INVALID_ARGUMENT:
         raise RuntimeError("stretch_error: approximate distance below exact (engine bug)")
@@ -501,12 +532,29 @@ class Exchange:
             self.handle = C.c_void_p()
 
 
+class DeviceView:
+    """Non-owning double[n] device array, e.g. DeviceGraph.last_projection()
+    (valid until the graph's next run; DeviceBuffer.copy keeps it)."""
+
+    def __init__(self, ptr, n: int):
+        self.ptr = ptr
+        self.n = int(n)
+        self.nbytes = 8 * self.n
+
+
 class DeviceBuffer:
     """Device memory owned by libggb (gg_device_upload / gg_bp_priors_device)."""
 
     def __init__(self, ptr, nbytes: int):
         self.ptr = ptr
         self.nbytes = int(nbytes)
+        self.n = self.nbytes // 8
+
+    @classmethod
+    def copy(cls, view) -> "DeviceBuffer":
+        h = C.c_void_p()
+        _raise(L.lib().gg_device_copy(view.ptr, view.nbytes, C.byref(h)), None)
+        return cls(h, view.nbytes)
 
     @classmethod
     def upload(cls, array: np.ndarray) -> "DeviceBuffer":

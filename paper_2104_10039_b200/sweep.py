@@ -142,9 +142,12 @@ def run_sweep(plan: SweepPlan, runner=None) -> list:
         raise ValueError("sweep grids must be non-empty")
     program, graph, project = _program_and_projection(plan)
     n = graph.n
-    if runner is None:  # device engine: upload the graph once for all cells
+    dev = None
+    if runner is None:  # device engine: upload the graph once for all cells;
+        # properties stay in HBM and the metric runs on the GPU (metrics.cu)
         dev = E.DeviceGraph.upload(graph)
-        runner = lambda _g, p, c: E.run(dev, p, c)  # noqa: E731
+        runner = lambda _g, p, c: E.run(dev, p, c, device_output=True)  # noqa: E731
+        project = lambda _p: dev.last_projection()  # noqa: E731
     metric = plan.metric_override or default_metric(plan.algo)
     k = plan.topk if plan.topk > 0 else max(1, n // 100)
     budget = plan.iterations if plan.iterations > 0 else default_iteration_budget(plan.algo, n)
@@ -155,8 +158,11 @@ def run_sweep(plan: SweepPlan, runner=None) -> list:
         for _ in range(plan.repeats):
             rep = runner(graph, program, cfg)
             wall += rep.total_wall_seconds
-        refs.append((project(rep.final_properties), rep.iterations_run,
-                     rep.total_processed_edges, wall / plan.repeats * 1e3))
+        exact = project(rep.final_properties)
+        if dev is not None:
+            exact = E.DeviceBuffer.copy(exact)  # outlives the next run
+        refs.append((exact, rep.iterations_run, rep.total_processed_edges,
+                     wall / plan.repeats * 1e3))
     ref_iters = refs[0][1]
     ref_wall = sum(r[3] for r in refs) / len(refs)
     rows = [SweepRow("accurate", 1.0, 0.0, 0, ref_iters, plan.repeats, 100.0, 1.0, 1.0, ref_wall,
@@ -178,6 +184,10 @@ def run_sweep(plan: SweepPlan, runner=None) -> list:
                        ratio_sum / ns, wall_sum / ns, ref_wall)
         row.speedup = ref_wall / row.wall_ms_mean if row.wall_ms_mean > 0 else 1.0
         rows.append(row)
+    if dev is not None:
+        for r in refs:
+            r[0].close()
+        dev.close()
     return rows
 
 
