@@ -158,6 +158,15 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
 /* Copy the (full, single-rank) CSC back to host buffers (any may be NULL). */
 gg_status gg_dev_graph_export(const gg_dev_graph* g, uint64_t* offsets, uint32_t* sources,
                               void* weights, uint32_t* out_degree);
+/* Binary CSC files straight to HBM (graph.cpp:259-300). Reads the
+ * reference's GGCSR1 (u64 sources) and GGCSR2 (u32 sources, weight kind,
+ * stored out-degrees); errors name the file like read_binary. Save writes
+ * GGCSR2 from a single-rank graph. */
+gg_status gg_dev_graph_load(const char* path, const gg_part_opts* opts, gg_dev_graph** out,
+                            gg_error* err);
+gg_status gg_dev_graph_save(const gg_dev_graph* g, const char* path, gg_error* err);
+/* Weight storage of a resident graph (gg_weight_kind), -1 for a null graph. */
+int32_t gg_dev_graph_weight_kind(const gg_dev_graph* g);
 /* BASELINE C4 priors generated on device (float[2n]); copied to host if out != NULL. */
 gg_status gg_bp_priors(uint64_t n, uint64_t seed, float* out);
 /* ... or left in device memory (*dev_out, free with gg_device_free). */

@@ -391,6 +391,10 @@ class Reference:
             L.ref_symmetrized.restype = C.c_void_p
             L.ref_graph_arrays.argtypes = [C.c_void_p, u64p, u32p, C.c_void_p, u32p]
             L.ref_graph_weighted.argtypes = [C.c_void_p]
+            L.ref_write_binary.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]
+            L.ref_read_binary.argtypes = [C.c_char_p, C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
+            L.ref_read_binary.restype = C.c_void_p
             L.ref_metric.argtypes = [C.c_int, f64p, f64p, C.c_uint64, C.c_uint64,
                                      C.POINTER(C.c_double)]
             L.ref_sweep_csv.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int, f64p, C.c_int,
@@ -438,6 +442,27 @@ class Reference:
         h0 = cls.graph(g)
         h = cls.lib().ref_symmetrized(h0, C.byref(n), C.byref(e))
         cls.free(h0)
+        return cls._export(h, n.value, e.value)
+
+    @classmethod
+    def write_binary(cls, g: CSC, path: str):
+        """The reference's GGCSR1 writer (graph.cpp:259-270)."""
+        msg = C.create_string_buffer(256)
+        h = cls.graph(g)
+        rc = cls.lib().ref_write_binary(h, path.encode(), msg, 256)
+        cls.free(h)
+        if rc:
+            raise RuntimeError(msg.value.decode())
+
+    @classmethod
+    def read_binary(cls, path: str) -> CSC:
+        """The reference's GGCSR1 reader (graph.cpp:272-296); RuntimeError with
+        its message on a bad file."""
+        n, e = C.c_uint64(), C.c_uint64()
+        msg = C.create_string_buffer(256)
+        h = cls.lib().ref_read_binary(path.encode(), C.byref(n), C.byref(e), msg, 256)
+        if not h:
+            raise RuntimeError(msg.value.decode())
         return cls._export(h, n.value, e.value)
 
     @classmethod

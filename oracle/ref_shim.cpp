@@ -265,6 +265,30 @@ int ref_run(const void* graph, int prog, const ref_params* p, const ref_config* 
     return 0;
 }
 
+// GGCSR1 files through the reference's own writer / reader (graph.cpp:259-300).
+int ref_write_binary(const void* graph, const char* path, char* msg, std::size_t msg_cap) {
+    try {
+        gg::write_binary(*static_cast<const gg::Graph*>(graph), path);
+        return 0;
+    } catch (const std::exception& e) {
+        copy_msg(msg, msg_cap, e.what());
+        return 1;
+    }
+}
+
+void* ref_read_binary(const char* path, std::uint64_t* n, std::uint64_t* e, char* msg,
+                      std::size_t msg_cap) {
+    try {
+        auto* g = new gg::Graph(gg::read_binary(path));
+        *n = g->num_vertices();
+        *e = g->num_edges();
+        return g;
+    } catch (const std::exception& ex) {
+        copy_msg(msg, msg_cap, ex.what());
+        return nullptr;
+    }
+}
+
 int ref_sparsify(const void* graph, double sigma, std::uint64_t seed, std::uint8_t* out) {
     try {
         gg::EdgeFlags f = gg::sparsify(*static_cast<const gg::Graph*>(graph), sigma, seed);

@@ -15,7 +15,8 @@ GG_W_NONE, GG_W_U32, GG_W_F32, GG_W_F64 = range(4)
 EXPORTS = (
     "gg_status_string", "gg_abi_version", "gg_bp_priors_device", "gg_device_upload",
     "gg_device_free", "gg_device_copy", "gg_last_projection", "gg_topk_error_dev",
-    "gg_relative_error_dev", "gg_stretch_error_dev", "gg_dev_graph_create", "gg_dev_graph_destroy",
+    "gg_relative_error_dev", "gg_stretch_error_dev", "gg_dev_graph_load", "gg_dev_graph_save",
+    "gg_dev_graph_weight_kind", "gg_dev_graph_create", "gg_dev_graph_destroy",
     "gg_dev_graph_info", "gg_dev_graph_create_rmat", "gg_dev_graph_export", "gg_bp_priors",
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
@@ -116,6 +117,10 @@ def lib():
     L.gg_device_upload.argtypes = [vp, C.c_uint64, P(vp)]
     L.gg_device_free.argtypes = [vp]
     L.gg_device_copy.argtypes = [vp, C.c_uint64, P(vp)]
+    L.gg_dev_graph_load.argtypes = [C.c_char_p, P(PartOpts), P(vp), P(ErrorC)]
+    L.gg_dev_graph_save.argtypes = [vp, C.c_char_p, P(ErrorC)]
+    L.gg_dev_graph_weight_kind.argtypes = [vp]
+    L.gg_dev_graph_weight_kind.restype = C.c_int32
     L.gg_last_projection.argtypes = [vp, P(vp)]
     L.gg_topk_error_dev.argtypes = [vp, vp, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.gg_relative_error_dev.argtypes = [vp, vp, C.c_uint64, P(C.c_double)]

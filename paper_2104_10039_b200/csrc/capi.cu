@@ -34,7 +34,7 @@ __global__ void rebase_kernel(const uint64_t* __restrict__ in, uint64_t count, u
         out[i] = in[i] - base;
 }
 
-static void setup_common(DevGraph& g, const gg_part_opts* opts) {
+void setup_common(DevGraph& g, const gg_part_opts* opts) {
     int dev = 0;
     if (opts && opts->device >= 0) dev = opts->device;
     else GGB_CUDA(cudaGetDevice(&dev));
@@ -68,7 +68,7 @@ static void setup_common(DevGraph& g, const gg_part_opts* opts) {
     if (g.rank < 0 || g.rank >= g.nranks) throw Error(GG_INVALID_ARGUMENT, "rank out of range");
 }
 
-static void finish_graph(DevGraph& g, const uint64_t* host_off_full) {
+void finish_graph(DevGraph& g, const uint64_t* host_off_full) {
     g.bounds = plan_partition(g.n, host_off_full, g.nranks);
     g.ebounds.resize(g.nranks + 1);
     for (int r = 0; r <= g.nranks; ++r) g.ebounds[r] = host_off_full[g.bounds[r]];

@@ -126,6 +126,9 @@ struct DevGraph {
 };
 
 size_t weight_size(gg_weight_kind k);
+// graph creation steps shared by the C-ABI constructors (capi.cu)
+void setup_common(DevGraph& g, const gg_part_opts* opts);
+void finish_graph(DevGraph& g, const uint64_t* host_off_full);
 
 // A full CSC generated on device (rmat.cu).
 struct RmatCsc {

@@ -15,6 +15,7 @@ std::invalid_argument -> ValueError and gg::EngineError -> EngineError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 
@@ -130,6 +131,28 @@ class DeviceGraph:
         _raise(L.lib().gg_dev_graph_create(C.byref(view), C.byref(opts), C.byref(h), C.byref(err)),
                err)
         return cls(h, g.n, g.num_edges())
+
+    @classmethod
+    def load(cls, path, device: int = -1, rank: int = 0, nranks: int = 1, exchange=None):
+        """Binary CSC file (reference GGCSR1 or GGCSR2) streamed straight to HBM."""
+        opts = L.PartOpts(device, rank, nranks, exchange)
+        h = C.c_void_p()
+        err = L.ErrorC()
+        rc = L.lib().gg_dev_graph_load(os.fsencode(path), C.byref(opts), C.byref(h), C.byref(err))
+        if rc == L.GG_INVALID_ARGUMENT:
+            raise RuntimeError(err.msg.decode())  # read_binary throws std::runtime_error
+        _raise(rc, err)
+        n, e = C.c_uint64(), C.c_uint64()
+        L.lib().gg_dev_graph_info(h, C.byref(n), C.byref(e), None, None, None)
+        dg = cls(h, n.value, e.value)
+        dg.weight_dtype = {L.GG_W_U32: np.uint32, L.GG_W_F32: np.float32,
+                           L.GG_W_F64: np.float64}.get(L.lib().gg_dev_graph_weight_kind(h))
+        return dg
+
+    def save(self, path):
+        """GGCSR2 file (u32 sources, weight kind, out-degrees)."""
+        err = L.ErrorC()
+        _raise(L.lib().gg_dev_graph_save(self._h, os.fsencode(path), C.byref(err)), err)
 
     def last_projection(self) -> "DeviceView":
         """double[n] device projection of the last run (PR rank, SSSP distance,
