@@ -543,51 +543,81 @@ vertex_kernel(const VertexArgs<P, W> a) {
     using Property = typename P::Property;
     unsigned long long g = 0, pcount = 0;
     unsigned int changed = 0, inv = 0, bad = 0xffffffffu;
-    for (uint32_t lv = blockIdx.x * blockDim.x + threadIdx.x; lv < a.nloc;
-         lv += gridDim.x * blockDim.x) {
-        const uint32_t v = a.v_begin + lv;
-        const uint32_t sv = a.slot_of[v];
-        const uint8_t st = a.st_cur[lv];
-        const uint64_t o0 = a.off[lv], o1 = a.off[lv + 1];
-        const bool proc = (st & kStActive) || a.a_off[lv + 1] > a.a_off[lv];
-        const Property prev = a.prop[lv];
-        if (proc) {
-            Accum acc = a.prog.gather_identity();
-            if (o1 > o0) {
-                const uint64_t t0 = (o0 + a.pad) / kChunkEdges, t1 = (o1 - 1 + a.pad) / kChunkEdges;
-                if (t0 == t1) {
-                    acc = a.acc_out[lv];
-                } else {
-                    acc = a.tv[t0];
-                    for (uint64_t t = t0 + 1; t <= t1; ++t) {
-                        if constexpr (SUPER) a.carry[t] = acc;
-                        acc = a.prog.combine(acc, a.hv[t]);
+    // U vertices per thread per step, every load of the step issued before
+    // any use (the accumulator of a single-task vertex is read speculatively):
+    // one memory latency per U vertices instead of a dependent chain each.
+#ifndef GGB_VERTEX_UNROLL
+#define GGB_VERTEX_UNROLL 2
+#endif
+    constexpr int U = (sizeof(Accum) + sizeof(Property) <= 16) ? GGB_VERTEX_UNROLL : 2;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < a.nloc; base += U * stride) {
+        uint8_t st[U];
+        uint64_t o0[U], o1[U], q0[U], q1[U];
+        uint32_t sv[U], deg[U];
+        Property prev[U];
+        Accum acc1[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+            const uint32_t lv = base + i * stride;
+            if (lv < a.nloc) {
+                const uint32_t v = a.v_begin + lv;
+                sv[i] = a.slot_of[v];
+                st[i] = a.st_cur[lv];
+                o0[i] = a.off[lv];
+                o1[i] = a.off[lv + 1];
+                q0[i] = a.a_off[lv];
+                q1[i] = a.a_off[lv + 1];
+                prev[i] = a.prop[lv];
+                acc1[i] = a.acc_out[lv];
+                deg[i] = 0;
+                if constexpr (P::kNeedsDegree) deg[i] = a.outdeg[v];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+            const uint32_t lv = base + i * stride;
+            if (lv >= a.nloc) continue;
+            const uint32_t v = a.v_begin + lv;
+            const bool proc = (st[i] & kStActive) || q1[i] > q0[i];  // engine.hpp:196
+            if (proc) {
+                Accum acc = a.prog.gather_identity();
+                if (o1[i] > o0[i]) {
+                    const uint64_t t0 = (o0[i] + a.pad) / kChunkEdges,
+                                   t1 = (o1[i] - 1 + a.pad) / kChunkEdges;
+                    if (t0 == t1) {
+                        acc = acc1[i];
+                    } else {
+                        acc = a.tv[t0];
+                        for (uint64_t t = t0 + 1; t <= t1; ++t) {
+                            if constexpr (SUPER) a.carry[t] = acc;
+                            acc = a.prog.combine(acc, a.hv[t]);
+                        }
                     }
                 }
+                const Property fresh = a.prog.apply(v, acc, prev[i], a.n);  // GG-Apply (:216)
+                const bool active = a.prog.vstatus(prev[i], fresh);         // GG-VStatus (:217)
+                const bool ok = a.prog.valid(fresh);                        // (:218)
+                a.prop[lv] = fresh;
+                a.msg_next[sv[i]] = a.prog.message(fresh, deg[i]);
+                a.st_next[lv] =
+                    (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
+                g += o1[i] - o0[i];
+                pcount += 1;
+                changed |= active ? 1u : 0u;
+                if (!ok) {
+                    inv = 1;
+                    // outside supersteps the reference's scan condition
+                    // (status || active_in_degree > 0, engine.hpp:229) is exactly
+                    // "processed"; supersteps are re-checked after the rebuild.
+                    if (!SUPER) bad = min(bad, v);
+                }
+            } else {
+                // skipped: next = prev (engine.hpp:183), status 0. The message
+                // buffers only differ if the vertex was processed last iteration.
+                if (st[i] & kStProcessed) a.msg_next[sv[i]] = a.msg_cur[sv[i]];
+                a.st_next[lv] = 0;
             }
-            const Property fresh = a.prog.apply(v, acc, prev, a.n);  // GG-Apply (:216)
-            const bool active = a.prog.vstatus(prev, fresh);         // GG-VStatus (:217)
-            const bool ok = a.prog.valid(fresh);                     // (:218)
-            a.prop[lv] = fresh;
-            uint32_t deg = 0;
-            if constexpr (P::kNeedsDegree) deg = a.outdeg[v];
-            a.msg_next[sv] = a.prog.message(fresh, deg);
-            a.st_next[lv] = (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
-            g += o1 - o0;
-            pcount += 1;
-            changed |= active ? 1u : 0u;
-            if (!ok) {
-                inv = 1;
-                // outside supersteps the reference's scan condition
-                // (status || active_in_degree > 0, engine.hpp:229) is exactly
-                // "processed"; supersteps are re-checked after the rebuild.
-                if (!SUPER) bad = min(bad, v);
-            }
-        } else {
-            // skipped: next = prev (engine.hpp:183), status 0. The message
-            // buffers only differ if the vertex was processed last iteration.
-            if (st & kStProcessed) a.msg_next[sv] = a.msg_cur[sv];
-            a.st_next[lv] = 0;
         }
     }
     // block reduction, one atomic per counter per block
