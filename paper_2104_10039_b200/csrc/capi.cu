@@ -12,6 +12,8 @@
 namespace ggb {
 
 // 32-aligned, edge-balanced destination ranges.
+constexpr uint64_t kPartAlign = 32;  // rank ranges start at multiples of 32 vertices
+
 static std::vector<uint64_t> plan_partition(uint64_t n, const uint64_t* off, int nranks) {
     std::vector<uint64_t> b(nranks + 1, 0);
     b[nranks] = n;
@@ -19,7 +21,7 @@ static std::vector<uint64_t> plan_partition(uint64_t n, const uint64_t* off, int
     for (int r = 1; r < nranks; ++r) {
         const uint64_t target = (uint64_t)((long double)e * r / nranks);
         uint64_t v = (uint64_t)(std::lower_bound(off, off + n + 1, target) - off);
-        v = (v / kWindow) * kWindow;
+        v = (v / kPartAlign) * kPartAlign;
         if (v < b[r - 1]) v = b[r - 1];
         if (v > n) v = n;
         b[r] = v;

@@ -18,14 +18,9 @@
 namespace ggb {
 
 constexpr int kWarp = 32;
-constexpr int kWindow = 32;              // vertices per window (one per lane)
 constexpr int kRun = 16;                 // consecutive in-edges folded by one lane
 constexpr int kChunkEdges = kWarp * kRun;  // in-edges per warp task (512)
-constexpr int kRowsPerChunk = kChunkEdges / 32;
-#ifndef GGB_EDGE_BLOCK_THREADS
-#define GGB_EDGE_BLOCK_THREADS 128
-#endif
-constexpr int kBlockThreads = GGB_EDGE_BLOCK_THREADS;
+constexpr int kBlockThreads = 128;       // edge kernels: 4 warps per CTA
 constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 
 // splitmix64 finalizer: engine.cpp:9-14 (bit-identical on host and device).
@@ -124,9 +119,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
-}
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
 }
 // Streaming (read-once) 32-bit load: bypass L1, evict-first in L2.
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
@@ -312,68 +304,15 @@ struct WarpRows {
     }
 };
 
-// ---- cp.async (LDGSTS): global -> shared without registers, so one warp can
-// keep hundreds of independent gathers in flight.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-template <int BYTES>
-__device__ __forceinline__ void cp_async(void* smem, const void* gmem, uint64_t pol) {
-    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
-    if constexpr (BYTES == 16)
-        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                     :: "r"(smem_u32(smem)), "l"(gmem), "l"(pol) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;"
-                     :: "r"(smem_u32(smem)), "l"(gmem), "n"(BYTES), "l"(pol) : "memory");
-}
-// Copy one trivially copyable element of any 4-byte-granular size.
-template <class T>
-__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem, uint64_t pol) {
-    static_assert(sizeof(T) % 4 == 0, "4-byte granular");
-    char* d = reinterpret_cast<char*>(smem);
-    const char* s = reinterpret_cast<const char*>(gmem);
-    if constexpr (sizeof(T) % 16 == 0) {
-#pragma unroll
-        for (int i = 0; i < (int)(sizeof(T) / 16); ++i) cp_async<16>(d + 16 * i, s + 16 * i, pol);
-    } else if constexpr (sizeof(T) % 8 == 0) {
-#pragma unroll
-        for (int i = 0; i < (int)(sizeof(T) / 8); ++i) cp_async<8>(d + 8 * i, s + 8 * i, pol);
-    } else {
-#pragma unroll
-        for (int i = 0; i < (int)(sizeof(T) / 4); ++i) cp_async<4>(d + 4 * i, s + 4 * i, pol);
-    }
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 
-// L2-coherent load of data written by other CTAs in the same kernel
-// (after their __threadfence + ticket atomic).
-template <class T>
-__device__ __forceinline__ T ld_cg_any(const T* p) {
-    static_assert(sizeof(T) % 4 == 0, "32-bit granular types only");
-    T out;
-    int* dst = reinterpret_cast<int*>(&out);
-    const int* src = reinterpret_cast<const int*>(p);
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(T) / 4); ++i) dst[i] = __ldcg(src + i);
-    return out;
-}
-
-template <class W>
-struct WeightIO {
-    __device__ static double load(const W* w, uint64_t e) { return (double)__ldg(w + e); }
-};
-template <>
-struct WeightIO<void> {
-    __device__ static double load(const void*, uint64_t) { return 1.0; }
-};
 template <class W>
 constexpr int weight_bytes() { return sizeof(W); }
 template <>
