@@ -108,3 +108,18 @@ def test_ranks_all_schemes_pagerank(ggb, scheme):
     single = ggb.run(graph, program, cfg)
     for rep in _run_ranks(ggb, graph, program, cfg, 4):
         _same(rep, single)
+
+
+@pytest.mark.parametrize("nranks", [3, 5])
+def test_ranks_with_tiny_and_empty_slices(ggb, nranks):
+    """Ranks whose 32-aligned slice is empty or holds no edges (a 70-vertex
+    graph over 5 ranks) still take part in every exchange."""
+    g = Oracle.power_law(70, 3.0, 2.0, 11)
+    graph = ggb.Graph(g.n, g.off, g.src, None, g.outdeg)
+    plan = ggb.partition_plan(graph, nranks)
+    assert any(plan[r + 1] == plan[r] for r in range(nranks)), plan  # some rank is empty
+    for prog in (ggb.pagerank_spec(0.85, 1e-7), ggb.wcc_spec()):
+        cfg = ggb.EngineConfig("gg", 0.5, 0.01, 2, 20, 3)
+        single = ggb.run(graph, prog, cfg)
+        for rep in _run_ranks(ggb, graph, prog, cfg, nranks):
+            _same(rep, single)
