@@ -103,6 +103,15 @@ class ClockSampler:
             if len(parts) >= 7:
                 rows.append(parts)
         os.unlink(self.path)
+        if not rows:  # region shorter than the sampling period: one immediate sample
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=10).stdout
+                rows = [[p.strip() for p in line.split(",")] for line in out.splitlines()
+                        if len(line.split(",")) >= 7]
+            except Exception:
+                rows = []
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         loaded = [r for r in rows if r[6].isdigit() and int(r[6]) > 0] or rows
