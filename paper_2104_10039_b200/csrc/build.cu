@@ -290,6 +290,18 @@ __global__ void relabel_kernel(uint32_t* __restrict__ src, uint64_t count,
         src[i] = __ldg(slot_of + src[i]);
 }
 
+__global__ void gathered_count_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
+                                      const uint64_t* __restrict__ bounds, int nranks,
+                                      unsigned long long* __restrict__ cnt) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        if (!outdeg[v]) continue;
+        int r = 0;
+        while (r + 1 < nranks && v >= bounds[r + 1]) ++r;
+        atomicAdd(cnt + r, 1ull);
+    }
+}
+
 void compute_slots(DevGraph& g) {
     const uint64_t n = g.n;
     g.slot_of = static_cast<decltype(g.slot_of)>(dev_alloc((n + 1) * 4, g.stream));
@@ -317,6 +329,17 @@ void compute_slots(DevGraph& g) {
                                              g.stream));
     slot_fill_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(v1, n, g.slot_of, g.vtx_of_slot);
     GGB_CUDA(cudaGetLastError());
+    if (g.nranks > 1) {  // per-rank gathered-slot counts for the message exchange
+        auto* cnt = static_cast<unsigned long long*>(dev_alloc(8 * g.nranks, g.stream));
+        GGB_CUDA(cudaMemsetAsync(cnt, 0, 8 * g.nranks, g.stream));
+        gathered_count_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, cnt);
+        GGB_CUDA(cudaGetLastError());
+        g.gathered_slots.assign(g.nranks, 0);
+        GGB_CUDA(cudaMemcpyAsync(g.gathered_slots.data(), cnt, 8 * g.nranks, cudaMemcpyDeviceToHost,
+                                 g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        dev_free(cnt, g.stream);
+    }
     dev_free(k0, g.stream); dev_free(k1, g.stream); dev_free(v0, g.stream); dev_free(v1, g.stream); dev_free(db, g.stream); dev_free(tmpp, g.stream);
 }
 

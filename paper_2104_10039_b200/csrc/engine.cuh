@@ -360,7 +360,7 @@ struct Engine {
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
                 if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
-                exchange_slices(g, msg[cur ^ 1], sizeof(Msg));
+                exchange_slices(g, msg[cur ^ 1], sizeof(Msg), /*slots=*/true);
                 exchange_counters(g, ctr);
                 if (timing) GGB_CUDA(cudaEventRecord(e7, g.stream));
             }

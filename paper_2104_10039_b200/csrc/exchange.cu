@@ -68,12 +68,19 @@ struct LocalGroup {
     }
 };
 
-static void local_slices(DevGraph& g, LocalGroup& L, void* buf, size_t elem) {
+// element range of rank r's slice
+static inline void slice_of(const DevGraph& g, int r, bool slots, uint64_t& b, uint64_t& e) {
+    b = g.bounds[r];
+    e = slots && !g.gathered_slots.empty() ? b + g.gathered_slots[r] : g.bounds[r + 1];
+}
+
+static void local_slices(DevGraph& g, LocalGroup& L, void* buf, size_t elem, bool slots) {
     GGB_CUDA(cudaStreamSynchronize(g.stream));  // this rank's slice is written
     L.bufs[g.rank] = buf;
     L.barrier();
     for (int r = 0; r < g.nranks; ++r) {
-        const uint64_t b = g.bounds[r], e = g.bounds[r + 1];
+        uint64_t b, e;
+        slice_of(g, r, slots, b, e);
         if (r == g.rank || e == b) continue;
         GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(buf) + b * elem,
                                  static_cast<const char*>(L.bufs[r]) + b * elem, (e - b) * elem,
@@ -90,14 +97,16 @@ static void nccl_check(ncclResult_t r, const char* what) {
     }
 }
 
-void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size) {
+void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots) {
     if (g.nranks <= 1) return;
-    if (g.exchange && g.exchange->local) return local_slices(g, *g.exchange->local, global_buf, elem_size);
+    if (g.exchange && g.exchange->local)
+        return local_slices(g, *g.exchange->local, global_buf, elem_size, slots);
     if (!g.exchange || !g.exchange->comm) throw Error(GG_NCCL, "multi-rank graph without exchange");
     const NcclApi& api = nccl();
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (int r = 0; r < g.nranks; ++r) {
-        const uint64_t b = g.bounds[r], e = g.bounds[r + 1];
+        uint64_t b, e;
+        slice_of(g, r, slots, b, e);
         if (e == b) continue;
         char* p = static_cast<char*>(global_buf) + b * elem_size;
         nccl_check(api.Broadcast(p, p, (e - b) * elem_size, ncclChar, r, g.exchange->comm, g.stream),

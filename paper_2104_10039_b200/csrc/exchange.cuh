@@ -41,7 +41,10 @@ struct NcclApi {
 };
 const NcclApi& nccl();
 
-void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size);
+// All-gather of each rank's slice of a global array. slots = true: the
+// array is in message-slot order and only the slots that are ever gathered
+// (out-degree > 0, a prefix of each rank's slot range) travel.
+void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots = false);
 void exchange_counters(DevGraph& g, void* ctr);
 // sum of `local` over ranks below this one (allgather of one u64 per rank)
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local);

@@ -105,6 +105,9 @@ struct DevGraph {
     // into L2; src arrays hold slot ids. slot_of[v] / vtx_of_slot[s], global.
     uint32_t* slot_of = nullptr;
     uint32_t* vtx_of_slot = nullptr;
+    // per rank: how many of its slots have out-degree > 0 (a prefix of its
+    // slot range, the only messages any gather reads; exchange_slices)
+    std::vector<uint64_t> gathered_slots;
     ListMeta full;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
