@@ -409,4 +409,13 @@ DevGraph::~DevGraph() {
     }
 }
 
+__global__ void reset_counters_kernel(IterCounters* __restrict__ c, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        IterCounters z{};
+        z.bad_min = 0xffffffffu;
+        c[i] = z;
+    }
+}
+
 }  // namespace ggb

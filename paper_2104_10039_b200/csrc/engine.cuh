@@ -183,8 +183,13 @@ struct Engine {
         Msg* msg[2] = {ws.get<Msg>("msg0", n), ws.get<Msg>("msg1", n)};
         Prop* prop = ws.get<Prop>("prop", nloc + 1);
         uint8_t* st[2] = {ws.get<uint8_t>("st0", nloc + 1), ws.get<uint8_t>("st1", nloc + 1)};
-        IterCounters* ctr = ws.get<IterCounters>("ctr", 1);
+        // Counters are double-buffered: iteration t accumulates into ctr2[t & 1]
+        // and its vertex kernel resets ctr2[(t + 1) & 1] for the next one (the
+        // host has read it by then), so no memset is enqueued per iteration.
+        IterCounters* ctr2 = ws.get<IterCounters>("ctr", 2);
         IterCounters* h_ctr = static_cast<IterCounters*>(g.host_counters(sizeof(IterCounters)));
+        reset_counters_kernel<<<1, 2, 0, g.stream>>>(ctr2, 2);
+        GGB_CUDA(cudaGetLastError());
         Acc* acc_out = ws.get<Acc>("acc_out", nloc + 1);
         const uint64_t ntask_cap = g.full.ntasks + 2;
         Acc* hv = ws.get<Acc>("hv", ntask_cap);
@@ -312,10 +317,10 @@ struct Engine {
             va.hv = hv;
             va.tv = tv;
             va.carry = carry;
+            IterCounters* ctr = ctr2 + (t & 1);
             va.ctr = ctr;
+            va.ctr_next = ctr2 + ((t + 1) & 1);
 
-            GGB_CUDA(cudaMemsetAsync(ctr, 0, sizeof(IterCounters), g.stream));
-            GGB_CUDA(cudaMemsetAsync(&ctr->bad_min, 0xff, 4, g.stream));
             if (timing) GGB_CUDA(cudaEventRecord(e0, g.stream));
             if (L.ntasks) {
                 // every edge of the sparsified list (and of the full list under

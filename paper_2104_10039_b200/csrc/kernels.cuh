@@ -53,6 +53,8 @@ struct IterCounters {
     unsigned int pad;
 };
 
+__global__ void reset_counters_kernel(IterCounters* __restrict__ c, int n);
+
 // edge kernel flavours
 enum : int {
     kEdgePlain = 0,  // every edge of the list belongs to a processed vertex
@@ -124,6 +126,7 @@ struct VertexArgs {
     const typename P::Accum* __restrict__ tv;
     typename P::Accum* __restrict__ carry;            // superstep: carry into task t
     IterCounters* __restrict__ ctr;
+    IterCounters* __restrict__ ctr_next;              // reset here for the next iteration
 };
 
 __device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t v) {
@@ -616,6 +619,11 @@ vertex_kernel(const VertexArgs<P, W> a) {
                 a.st_next[lv] = 0;
             }
         }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        IterCounters z{};
+        z.bad_min = 0xffffffffu;
+        *a.ctr_next = z;
     }
     // block reduction, one atomic per counter per block
 #pragma unroll
