@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "exchange.cuh"
 #include "programs.cuh"
 
 namespace ggb {
@@ -433,8 +434,21 @@ gg_status gg_run_sssp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_sss
             SsspU32 prog;
             prog.source = source;
             prog.graded = graded;
+            prog.overflow = g.ws.get<unsigned int>("sssp.overflow", 1);
+            GGB_CUDA(cudaMemsetAsync(prog.overflow, 0, 4, g.stream));
             if (g.wkind == GG_W_NONE) Engine<SsspU32, void>::run(g, prog, io);
             else Engine<SsspU32, uint32_t>::run(g, prog, io);
+            unsigned int ovf = 0;
+            GGB_CUDA(cudaMemcpyAsync(&ovf, prog.overflow, 4, cudaMemcpyDeviceToHost, g.stream));
+            GGB_CUDA(cudaStreamSynchronize(g.stream));
+            if (exchange_sum(g, ovf)) {  // a distance beyond u32: redo with f64 distances
+                SsspF64 p64;
+                p64.source = source;
+                p64.graded = graded;
+                io = make_io(cfg, recs, cap, sum, opts, out_props, 1);
+                if (g.wkind == GG_W_NONE) Engine<SsspF64, void>::run(g, p64, io);
+                else Engine<SsspF64, uint32_t>::run(g, p64, io);
+            }
         } else {
             SsspF64 prog;
             prog.source = source;

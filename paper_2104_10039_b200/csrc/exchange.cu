@@ -115,16 +115,16 @@ void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }
 
-uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
-    if (g.nranks <= 1) return 0;
+// every rank's `local` (allgather of one u64 per rank)
+static std::vector<uint64_t> exchange_all(DevGraph& g, uint64_t local) {
+    if (g.nranks <= 1) return {local};
     if (g.exchange && g.exchange->local) {
         LocalGroup& L = *g.exchange->local;
         L.vals[g.rank] = local;
         L.barrier();
-        uint64_t base = 0;
-        for (int r = 0; r < g.rank; ++r) base += L.vals[r];
+        std::vector<uint64_t> h(L.vals.begin(), L.vals.end());
         L.barrier();
-        return base;
+        return h;
     }
     const NcclApi& api = nccl();
     uint64_t* d = g.ws.get<uint64_t>("xbase", (uint64_t)g.nranks + 1);
@@ -137,9 +137,22 @@ uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
     std::vector<uint64_t> h(g.nranks);
     GGB_CUDA(cudaMemcpyAsync(h.data(), d, 8 * g.nranks, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
+    return h;
+}
+
+uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
+    if (g.nranks <= 1) return 0;
+    const std::vector<uint64_t> h = exchange_all(g, local);
     uint64_t base = 0;
     for (int r = 0; r < g.rank; ++r) base += h[r];
     return base;
+}
+
+uint64_t exchange_sum(DevGraph& g, uint64_t local) {
+    if (g.nranks <= 1) return local;
+    uint64_t s = 0;
+    for (uint64_t v : exchange_all(g, local)) s += v;
+    return s;
 }
 
 void exchange_counters(DevGraph& g, void* ctr_v) {

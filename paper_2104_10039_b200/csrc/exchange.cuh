@@ -48,5 +48,7 @@ void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots
 void exchange_counters(DevGraph& g, void* ctr);
 // sum of `local` over ranks below this one (allgather of one u64 per rank)
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local);
+// sum of `local` over all ranks
+uint64_t exchange_sum(DevGraph& g, uint64_t local);
 
 }  // namespace ggb

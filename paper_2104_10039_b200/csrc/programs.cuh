@@ -91,7 +91,9 @@ struct SsspF64 {
 // SsspProgram with u32 distances (BASELINE C2: u32 weights, or unit
 // weights). Integer sums are exact in f64, so every comparison and every
 // graded influence (computed in f64 from the exact integers) is bit-identical
-// to the f64 program. 0xffffffff encodes +inf.
+// to the f64 program. 0xffffffff encodes +inf. A candidate distance that does
+// not fit raises *overflow; the run is then repeated with SsspF64 (capi.cu),
+// so results stay those of the reference's f64 distances.
 struct SsspU32 {
     using Property = uint32_t;
     using Message = uint32_t;
@@ -101,6 +103,7 @@ struct SsspU32 {
     static constexpr uint32_t kInf = 0xffffffffu;
     uint32_t source = 0;
     bool graded = false;
+    unsigned int* overflow = nullptr;
 
     __device__ Property init_property(uint32_t v, uint64_t) const { return v == source ? 0u : kInf; }
     __device__ Accum gather_identity() const { return kInf; }
@@ -108,7 +111,8 @@ struct SsspU32 {
     __device__ double gather(Accum& acc, const Message& m, double w) const {
         if (m == kInf) return 0.0;  // inf + w < acc is false for every acc
         const uint64_t c64 = (uint64_t)m + (uint64_t)w;
-        const uint32_t cand = c64 >= kInf ? kInf - 1 : (uint32_t)c64;  // saturate (never hit for BASELINE sizes)
+        if (c64 >= kInf) *overflow = 1;  // the run is redone with f64 distances
+        const uint32_t cand = c64 >= kInf ? kInf - 1 : (uint32_t)c64;
         if (cand < acc) {
             double infl = 1.0;
             if (graded && acc != kInf) infl = ((double)acc - (double)cand) / (double)acc;

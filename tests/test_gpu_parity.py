@@ -196,6 +196,23 @@ def test_sssp_u32_weights_exact(ggb):
                 max_iterations=g.n + 1, source=src, graded=True, device_weights=w)
 
 
+def test_sssp_u32_weights_beyond_32_bit_distances(ggb):
+    """u32 weights whose path sums exceed 2^32-1: the u32-distance program
+    flags the overflow and the run is redone with f64 distances, so the
+    result still equals the reference's f64 arithmetic."""
+    g = Oracle.rmat(11, 8, 6)
+    rng = np.random.default_rng(6)
+    w = rng.integers(1 << 30, (1 << 32) - 1, g.e, dtype=np.uint64).astype(np.uint32)
+    gw = Oracle.build_graph(g.n, g.src, np.repeat(np.arange(g.n), np.diff(g.off.astype(np.int64))),
+                            w.astype(np.float64))
+    src = int(np.argmax(gw.outdeg))
+    for scheme in ("accurate", "gg"):
+        rep, ref, _ = compare(ggb, gw, SSSP, scheme=scheme, sigma=0.5, theta=0.05, alpha=4, seed=6,
+                              max_iterations=g.n + 1, source=src, graded=True, device_weights=w)
+        finite = np.asarray(ref.props)[np.isfinite(ref.props)]
+        assert finite.max() > 2 ** 32  # the overflow path was exercised
+
+
 def test_hub_windows_multi_chunk(ggb):
     # in-degree 5000 hub + 3000 hub: windows split into several chunks, and
     # the superstep hub pass evaluates their influences with chunk carries.
