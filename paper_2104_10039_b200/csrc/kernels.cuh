@@ -2,12 +2,20 @@
 //
 // Replaces the reference's iteration body (engine.hpp:177-241):
 //   edge_kernel    gather fold (GG-Gather, engine.hpp:198-213) over the
-//                  current list, influence + GG-EStatus into the active-edge
-//                  bitmap during supersteps (engine.hpp:204-211);
+//                  current list; in a superstep (kEdgeFoldStash) it also hands
+//                  every run's messages and prefixes to the influence pass;
+//   edge_kernel_hot the approximate fold with the hottest message slots in
+//                  shared memory (4-byte messages);
 //   vertex_kernel  skip test (:196), GG-Apply / GG-VStatus / valid (:216-224),
-//                  next = prev carry-over (:183), iteration counters;
-//   edge_pass2     superstep flags of edges whose vertex's fold began in an
-//                  earlier task (needs that task's carry).
+//                  next = prev carry-over (:183), iteration counters, and the
+//                  superstep carry into each task;
+//   edge_influence influence + GG-EStatus of every processed edge into the
+//                  active-edge bitmap (engine.hpp:204-211), streaming the
+//                  stash with the carried prefixes;
+//   kEdgeSuper + edge_pass2_kernel: the same superstep without the stash
+//                  (fallback when HBM cannot hold it): influences in the fold
+//                  kernel, re-gathering pass 2 for the vertices continuing
+//                  from an earlier task.
 //
 // Layout (per rank): the list (full or sparsified CSC) is addressed by PADDED
 // positions P = pad + local edge index, with pad chosen so that P equals the
