@@ -248,6 +248,24 @@ __device__ __forceinline__ void write_flags(uint32_t* __restrict__ bitmap, uint6
     }
 }
 
+// The superstep hand-over of one task's gathered messages to the stash:
+// warp-collective coalesced rows when the run is a power-of-two number of
+// 16-byte chunks, per-lane stores otherwise.
+template <class P, class W, class MA>
+__device__ __forceinline__ void stash_rows(const EdgeArgs<P, W>& a, char* xs, int lane, uint64_t t,
+                                           const MA& m) {
+    constexpr int RB = stash_row_bytes<P>();
+    if constexpr (RB != 0) {
+        uint4 row[RB / 16];
+        memcpy(row, &m[0], RB);
+        WarpRows<RB>::store(xs, lane, row, reinterpret_cast<uint4*>(a.stash + t * kChunkEdges));
+    } else {
+        const uint64_t P0 = (t * kWarp + lane) * kRun;
+#pragma unroll
+        for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
+    }
+}
+
 template <class P, class W, int MODE, bool PASS2, bool HOT = false>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, char* xs,
                                           uint64_t t, int lane, uint64_t pol_stream,
@@ -320,7 +338,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     uint32_t bmask = 0;  // positions where a later vertex of the run starts
     Accum x = a.prog.gather_identity(), hvv = x;
     bool head_closed = false;
-    for_run<P>([&](int j) {
+    auto fold_step = [&](int j, const Message& mj, double wj) {
         const int p = (int)(P0 - tstart) + j;
         if (p >= rlo && p < rhi) {
             if (p >= nb) {  // vertex k ended before p: next non-empty vertex
@@ -338,11 +356,29 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
             }
             if (pk) {
-                (void)a.prog.gather(x, m[j], wv(j));
+                (void)a.prog.gather(x, mj, wj);
                 pmask |= 1u << j;
             }
         }
-    });
+    };
+    // Heavy programs fold the run in a rolled loop (one inlined gather);
+    // without a second pass over the messages they shift the run through
+    // registers (element 0 each step) instead of indexing a local array.
+    constexpr bool kShift = fold_unroll<P>() == 1 && MODE != kEdgeSuper && !PASS2;
+    if constexpr (kShift) {
+        if constexpr (MODE == kEdgeFoldStash) stash_rows<P, W>(a, xs, lane, t, m);  // before the shifts
+#pragma unroll 1
+        for (int j = 0; j < kRun; ++j) {
+            fold_step(j, m[0], wv(0));
+#pragma unroll
+            for (int i = 0; i + 1 < kRun; ++i) {
+                m[i] = m[i + 1];
+                if constexpr (!std::is_void_v<W>) wr[i] = wr[i + 1];
+            }
+        }
+    } else {
+        for_run<P>([&](int j) { fold_step(j, m[j], wv(j)); });
+    }
     const uint32_t tk = len > 0 ? (uint32_t)k : 0x7fffff00u + (uint32_t)lane;  // unique when empty
     // join runs sharing a destination: segmented inclusive scan keyed by tk
     Accum S = x;
@@ -413,16 +449,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         if (lane == 0) a.task_info[t] = cont ? (kTaskCont | (uint32_t)st0[1]) : 0u;
         __stcs(a.run_meta + r, len > 0 ? (bmask | (pmask << 16)) : 0u);
         if (pmask) a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
-        constexpr int RB = stash_row_bytes<P>();
-        if constexpr (RB != 0) {  // warp-collective, coalesced
-            uint4 row[RB / 16];
-            memcpy(row, m, RB);
-            WarpRows<RB>::store(xs, lane, row,
-                                reinterpret_cast<uint4*>(a.stash + t * kChunkEdges));
-        } else if (pmask) {
-#pragma unroll
-            for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
-        }
+        if constexpr (!kShift) stash_rows<P, W>(a, xs, lane, t, m);
     }
     __syncwarp();  // st0 is restaged by the warp's next task
 }
