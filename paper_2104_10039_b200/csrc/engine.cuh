@@ -207,7 +207,15 @@ struct Engine {
             const size_t pbytes = (g.full.nruns + 1) * sizeof(Acc);
             const bool have = ws.bufs.count("stash") && ws.bufs["stash"].bytes >= sbytes;
             size_t free_b = 0, total_b = 0;
-            if (!have) GGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (!have) {  // free device memory + what the stream-ordered pool holds unused
+                GGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+                cudaMemPool_t pool;
+                uint64_t reserved = 0, used = 0;
+                GGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, g.device));
+                GGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+                GGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+                if (reserved > used) free_b += reserved - used;
+            }
             if (have || free_b > sbytes + pbytes + (4ull << 30)) {
                 stash = static_cast<Msg*>(ws.get("stash", sbytes));
                 lane_pre = ws.get<Acc>("lane_pre", g.full.nruns + 1);
