@@ -397,6 +397,7 @@ DevGraph::~DevGraph() {
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : bev) cudaEventDestroy(e);
     dev_free(off, stream);
     dev_free(src, stream);
     dev_free(w, stream);

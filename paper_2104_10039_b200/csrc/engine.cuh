@@ -139,6 +139,8 @@ struct Engine {
 
     // shared-memory hot-slot table of edge_kernel_hot (GGB_SMEM_HOT_KB, default
     // 160 KB; 0 disables the hot kernel)
+    static constexpr int kMaxBatch = 8;            // iterations enqueued per host sync
+    static constexpr int kRing = kMaxBatch + 1;    // counter slots
     static constexpr bool kHotOK =
         fold_unroll<P>() != 1 && (sizeof(Msg) == 4 || sizeof(Msg) == 8 || sizeof(Msg) == 16);
     // Measured (approximate gather, one B200): 4-byte messages gain 18% (c3
@@ -183,12 +185,14 @@ struct Engine {
         Msg* msg[2] = {ws.get<Msg>("msg0", n), ws.get<Msg>("msg1", n)};
         Prop* prop = ws.get<Prop>("prop", nloc + 1);
         uint8_t* st[2] = {ws.get<uint8_t>("st0", nloc + 1), ws.get<uint8_t>("st1", nloc + 1)};
-        // Counters are double-buffered: iteration t accumulates into ctr2[t & 1]
-        // and its vertex kernel resets ctr2[(t + 1) & 1] for the next one (the
-        // host has read it by then), so no memset is enqueued per iteration.
-        IterCounters* ctr2 = ws.get<IterCounters>("ctr", 2);
-        IterCounters* h_ctr = static_cast<IterCounters*>(g.host_counters(sizeof(IterCounters)));
-        reset_counters_kernel<<<1, 2, 0, g.stream>>>(ctr2, 2);
+        // Counters live in a ring of kRing slots: iteration u accumulates into
+        // ring[u % kRing] and its vertex kernel resets ring[(u + 1) % kRing]
+        // for the next one, so no memset is enqueued per iteration and a
+        // batch of up to kMaxBatch iterations is read back with one copy.
+        IterCounters* ring = ws.get<IterCounters>("ctr", kRing);
+        IterCounters* h_ring =
+            static_cast<IterCounters*>(g.host_counters(kRing * sizeof(IterCounters)));
+        reset_counters_kernel<<<1, kRing, 0, g.stream>>>(ring, kRing);
         GGB_CUDA(cudaGetLastError());
         Acc* acc_out = ws.get<Acc>("acc_out", nloc + 1);
         const uint64_t ntask_cap = g.full.ntasks + 2;
@@ -230,8 +234,6 @@ struct Engine {
         uint32_t* s_src = nullptr;
         void* s_w = nullptr;
         ListMeta sp;
-        cudaEvent_t e0 = timing ? g.event(0) : nullptr, e1 = timing ? g.event(1) : nullptr;
-        cudaEvent_t e2 = timing ? g.event(2) : nullptr, e3 = timing ? g.event(3) : nullptr;
         cudaEvent_t e4 = timing ? g.event(4) : nullptr, e5 = timing ? g.event(5) : nullptr;
         cudaEvent_t e6 = timing ? g.event(6) : nullptr, e7 = timing ? g.event(7) : nullptr;
 
@@ -272,11 +274,30 @@ struct Engine {
         int cur = 0;
         uint64_t iterations_run = 0, total_edges = 0;
         double total_wall = 0.0;
-        for (uint64_t t = 1; t <= cfg.max_iterations; ++t) {  // engine.hpp:177
+        // Iterations are enqueued in batches: a stretch of consecutive
+        // non-superstep iterations (one rank) is launched back to back with
+        // device-side early exit (stop_after) and read back with one sync;
+        // supersteps and multi-rank iterations form batches of one. Results
+        // and records are those of the one-at-a-time loop (engine.hpp:177-241).
+        auto batchable = [&](uint64_t u) {
+            return g.nranks == 1 && mode_for(cfg.scheme, u, cfg.alpha) != GG_MODE_SUPERSTEP;
+        };
+        bool done = false;
+        for (uint64_t t = 1; t <= cfg.max_iterations && !done;) {  // engine.hpp:177
             const auto t0 = std::chrono::steady_clock::now();
-            const int mode = mode_for(cfg.scheme, t, cfg.alpha);
+            int B = 1;
+            if (batchable(t))
+                while (t + B <= cfg.max_iterations && B < kMaxBatch && batchable(t + B)) ++B;
+            double rb_ms = 0.0;
+            bool super = false;
+            // timing events of batch member k (single iterations keep e0..e7)
+            auto ev = [&](int k, int i) { return B == 1 ? g.event(i) : g.batch_event(4 * k + i); };
+            for (int k = 0; k < B; ++k) {
+            const uint64_t u = t + k;
+            const int cu = cur ^ (k & 1);
+            const int mode = mode_for(cfg.scheme, u, cfg.alpha);
             const bool approx = mode == GG_MODE_APPROXIMATE;
-            const bool super = mode == GG_MODE_SUPERSTEP;
+            super = mode == GG_MODE_SUPERSTEP;
             const ListMeta& L = approx ? sp : g.full;
             EdgeArgs<P, W> ea{};
             ea.prog = prog;
@@ -291,8 +312,8 @@ struct Engine {
             ea.nruns = L.nruns;
             ea.nz = L.nz;
             ea.a_off = a_off;
-            ea.st_cur = st[cur];
-            ea.msg_cur = msg[cur];
+            ea.st_cur = st[cu];
+            ea.msg_cur = msg[cu];
             ea.hot_limit = hot_limit;
             ea.l2_limit = l2_limit;
             ea.cold_last = msgs_fit_l2 ? 1u : 0u;
@@ -306,6 +327,7 @@ struct Engine {
             ea.task_info = task_info;
             ea.bitmap = bitmap;
             ea.theta = cfg.theta;
+            ea.stop_if = k ? ring + (u - 1) % kRing : nullptr;
             VertexArgs<P, W> va{};
             va.prog = prog;
             va.n = n;
@@ -314,22 +336,23 @@ struct Engine {
             va.off = approx ? s_off : g.off;
             va.pad = L.pad;
             va.a_off = a_off;
-            va.st_cur = st[cur];
-            va.st_next = st[cur ^ 1];
+            va.st_cur = st[cu];
+            va.st_next = st[cu ^ 1];
             va.prop = prop;
-            va.msg_cur = msg[cur];
-            va.msg_next = msg[cur ^ 1];
+            va.msg_cur = msg[cu];
+            va.msg_next = msg[cu ^ 1];
             va.outdeg = g.outdeg;
             va.slot_of = g.slot_of;
             va.acc_out = acc_out;
             va.hv = hv;
             va.tv = tv;
             va.carry = carry;
-            IterCounters* ctr = ctr2 + (t & 1);
+            IterCounters* ctr = ring + u % kRing;
             va.ctr = ctr;
-            va.ctr_next = ctr2 + ((t + 1) & 1);
+            va.ctr_next = ring + (u + 1) % kRing;
+            va.stop_if = ea.stop_if;
 
-            if (timing) GGB_CUDA(cudaEventRecord(e0, g.stream));
+            if (timing) GGB_CUDA(cudaEventRecord(ev(k, 0), g.stream));
             if (L.ntasks) {
                 // every edge of the sparsified list (and of the full list under
                 // the accurate scheme) belongs to a processed vertex
@@ -343,12 +366,12 @@ struct Engine {
                 else launch_edge<kEdgeCheck>(g, ea);
                 ++launches;
             }
-            if (timing) GGB_CUDA(cudaEventRecord(e1, g.stream));
+            if (timing) GGB_CUDA(cudaEventRecord(ev(k, 1), g.stream));
             if (super) vertex_kernel<P, W, true><<<grid1d(nloc), 256, 0, g.stream>>>(va);
             else vertex_kernel<P, W, false><<<grid1d(nloc), 256, 0, g.stream>>>(va);
             GGB_CUDA(cudaGetLastError());
             ++launches;
-            if (timing) GGB_CUDA(cudaEventRecord(e2, g.stream));
+            if (timing) GGB_CUDA(cudaEventRecord(ev(k, 2), g.stream));
             if (super && L.ntasks) {  // flags of vertices whose fold began in an earlier task
                 if (stash)
                     edge_influence_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
@@ -357,66 +380,80 @@ struct Engine {
                 GGB_CUDA(cudaGetLastError());
                 ++launches;
             }
-            if (timing) GGB_CUDA(cudaEventRecord(e3, g.stream));
-            double rb_ms = 0.0;
+            if (timing) GGB_CUDA(cudaEventRecord(ev(k, 3), g.stream));
             if (super) {  // new flag set -> new sparsified CSC (engine.hpp:207-214)
                 kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, timing ? e4 : nullptr,
                                       timing ? e5 : nullptr, &launches);
-                GGB_CUDA(cudaMemcpyAsync(h_ctr, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
+                GGB_CUDA(cudaMemcpyAsync(h_ring, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
                                          g.stream));
                 GGB_CUDA(cudaStreamSynchronize(g.stream));
                 if (timing) rb_ms = event_ms(e4, e5);
-                if (h_ctr->any_invalid) {
-                    launch_superstep_invalid(g, st[cur], st[cur ^ 1], s_off, ctr);
+                if (h_ring->any_invalid) {
+                    launch_superstep_invalid(g, st[cu], st[cu ^ 1], s_off, ctr);
                     ++launches;
                 }
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
                 if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
-                exchange_slices(g, msg[cur ^ 1], sizeof(Msg), /*slots=*/true);
+                exchange_slices(g, msg[cu ^ 1], sizeof(Msg), /*slots=*/true);
                 exchange_counters(g, ctr);
                 if (timing) GGB_CUDA(cudaEventRecord(e7, g.stream));
             }
-            GGB_CUDA(cudaMemcpyAsync(h_ctr, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
-                                     g.stream));
+            }  // batch member k
+            GGB_CUDA(cudaMemcpyAsync(h_ring, ring, kRing * sizeof(IterCounters),
+                                     cudaMemcpyDeviceToHost, g.stream));
             GGB_CUDA(cudaStreamSynchronize(g.stream));
-            const double wall =
+            const double batch_wall =
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (h_ctr->bad_min != 0xffffffffu) {  // engine.hpp:226-233
-                Error e(GG_INVALID_PROPERTY,
-                        "invalid property at iteration " + std::to_string(t) + ", vertex " +
-                            std::to_string(h_ctr->bad_min));
-                e.iteration = t;
-                e.vertex = h_ctr->bad_min;
-                if (io.sum) {
-                    io.sum->iterations_run = iterations_run;
-                    io.sum->total_processed_edges = total_edges;
-                    io.sum->kernel_launches = (uint32_t)launches;
+            for (int k = 0; k < B; ++k) {
+                const uint64_t u = t + k;
+                const IterCounters& hc = h_ring[u % kRing];
+                const int mode = mode_for(cfg.scheme, u, cfg.alpha);
+                const bool approx = mode == GG_MODE_APPROXIMATE;
+                if (hc.bad_min != 0xffffffffu) {  // engine.hpp:226-233
+                    Error e(GG_INVALID_PROPERTY,
+                            "invalid property at iteration " + std::to_string(u) + ", vertex " +
+                                std::to_string(hc.bad_min));
+                    e.iteration = u;
+                    e.vertex = hc.bad_min;
+                    if (io.sum) {
+                        io.sum->iterations_run = iterations_run;
+                        io.sum->total_processed_edges = total_edges;
+                        io.sum->kernel_launches = (uint32_t)launches;
+                    }
+                    throw e;
                 }
-                throw e;
+                // host wall time: exact for single iterations, the batch's
+                // share for batch members (each member's GPU time is in the
+                // kernel fields when timing is on)
+                const double wall = batch_wall / B;
+                if (u - 1 < io.rec_cap && io.recs) {  // engine.hpp:235-236
+                    gg_iter_record& r = io.recs[u - 1];
+                    r.mode = mode;
+                    r.processed_edges = hc.gathered;
+                    r.active_vertices = hc.processed;
+                    r.wall_seconds = wall;
+                    r.edge_ms = timing ? event_ms(ev(k, 0), ev(k, 1)) + event_ms(ev(k, 2), ev(k, 3)) : 0.0;
+                    r.vertex_ms = timing ? event_ms(ev(k, 1), ev(k, 2)) : 0.0;
+                    r.kernel_ms = r.edge_ms + r.vertex_ms;
+                    r.rebuild_ms = rb_ms;
+                    r.exchange_ms = (timing && g.nranks > 1) ? event_ms(e6, e7) : 0.0;
+                    // per-rank algorithmic bytes of this rank's launches
+                    const uint64_t local_edges = approx ? kept : g.e_loc;
+                    r.edge_bytes = edge_bytes(local_edges, super);
+                    r.vertex_bytes = vertex_bytes(nloc);
+                    r.algo_bytes = r.edge_bytes + r.vertex_bytes;
+                }
+                iterations_run = u;
+                total_edges += hc.gathered;
+                total_wall += wall;
+                cur ^= 1;                               // engine.hpp:238-239
+                if (!hc.changed) {                      // engine.hpp:240
+                    done = true;
+                    break;
+                }
             }
-            if (t - 1 < io.rec_cap && io.recs) {  // engine.hpp:235-236
-                gg_iter_record& r = io.recs[t - 1];
-                r.mode = mode;
-                r.processed_edges = h_ctr->gathered;
-                r.active_vertices = h_ctr->processed;
-                r.wall_seconds = wall;
-                r.edge_ms = timing ? event_ms(e0, e1) + event_ms(e2, e3) : 0.0;
-                r.vertex_ms = timing ? event_ms(e1, e2) : 0.0;
-                r.kernel_ms = r.edge_ms + r.vertex_ms;
-                r.rebuild_ms = rb_ms;
-                r.exchange_ms = (timing && g.nranks > 1) ? event_ms(e6, e7) : 0.0;
-                // per-rank algorithmic bytes of this rank's launches
-                const uint64_t local_edges = approx ? kept : g.e_loc;
-                r.edge_bytes = edge_bytes(local_edges, super);
-                r.vertex_bytes = vertex_bytes(nloc);
-                r.algo_bytes = r.edge_bytes + r.vertex_bytes;
-            }
-            iterations_run = t;
-            total_edges += h_ctr->gathered;
-            total_wall += wall;
-            cur ^= 1;                               // engine.hpp:238-239
-            if (!h_ctr->changed) break;             // engine.hpp:240
+            t += B;
         }
 
         // final properties (engine.hpp:243)

@@ -117,6 +117,7 @@ struct DevGraph {
     std::function<const double*()> project_last;
     void* h_ctr = nullptr;            // pinned host mirror of the iteration counters
     cudaEvent_t ev[8] = {};           // timing events, created on first use
+    std::vector<cudaEvent_t> bev;     // timing events of batched iterations
     void* host_counters(size_t bytes) {
         if (!h_ctr) GGB_CUDA(cudaHostAlloc(&h_ctr, bytes, cudaHostAllocDefault));
         return h_ctr;
@@ -124,6 +125,14 @@ struct DevGraph {
     cudaEvent_t event(int i) {
         if (!ev[i]) GGB_CUDA(cudaEventCreate(&ev[i]));
         return ev[i];
+    }
+    cudaEvent_t batch_event(size_t i) {
+        while (bev.size() <= i) {
+            cudaEvent_t e;
+            GGB_CUDA(cudaEventCreate(&e));
+            bev.push_back(e);
+        }
+        return bev[i];
     }
     ~DevGraph();
 };

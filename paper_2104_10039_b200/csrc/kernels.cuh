@@ -63,6 +63,17 @@ struct IterCounters {
 
 __global__ void reset_counters_kernel(IterCounters* __restrict__ c, int n);
 
+// Device-side early exit inside a batch of enqueued iterations: the kernels
+// of iteration u+1 return at once when iteration u changed nothing or hit an
+// invalid property (engine.hpp:226-240). A skipped iteration leaves its
+// (zeroed) counters "unchanged", so the rest of the batch is skipped too.
+__device__ __forceinline__ bool stop_after(const IterCounters* prev) {
+    if (!prev) return false;
+    // written by an earlier kernel of the stream: the read-only path is
+    // coherent here, and every warp after the first per SM hits in L1
+    return __ldg(&prev->changed) == 0 || __ldg(&prev->bad_min) != 0xffffffffu;
+}
+
 // edge kernel flavours
 enum : int {
     kEdgePlain = 0,  // every edge of the list belongs to a processed vertex
@@ -112,6 +123,7 @@ struct EdgeArgs {
     uint32_t* __restrict__ task_info;  // [task] kTaskCont | end of the first vertex
     uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
     double theta;
+    const IterCounters* stop_if;            // batched iterations: the previous iteration's counters
 };
 
 template <class P, class W>
@@ -135,6 +147,7 @@ struct VertexArgs {
     typename P::Accum* __restrict__ carry;            // superstep: carry into task t
     IterCounters* __restrict__ ctr;
     IterCounters* __restrict__ ctr_next;              // reset here for the next iteration
+    const IterCounters* stop_if;                      // see EdgeArgs::stop_if
 };
 
 __device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t v) {
@@ -457,6 +470,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
 template <class P, class W, int MODE>
 __global__ void __launch_bounds__(kBlockThreads)
 edge_kernel(const EdgeArgs<P, W> a) {
+    if (stop_after(a.stop_if)) return;
     __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
     constexpr int RB = MODE == kEdgeFoldStash ? stash_row_bytes<P>() : 0;
     __shared__ __align__(16) char xs_all[kWarpsPerBlock][RB ? 32 * RB : 16];
@@ -480,6 +494,7 @@ constexpr int kHotWarps = 24;
 template <class P, class W, int MODE>
 __global__ void __launch_bounds__(kHotWarps * 32, 1)
 edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
+    if (stop_after(a.stop_if)) return;
     using Message = typename P::Message;
     extern __shared__ __align__(16) unsigned char hot_raw[];
     __shared__ int16_t st_all[kHotWarps][kStageStarts];
@@ -579,6 +594,12 @@ __global__ void __launch_bounds__(256)
 vertex_kernel(const VertexArgs<P, W> a) {
     using Accum = typename P::Accum;
     using Property = typename P::Property;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next iteration's counters, even if skipped
+        IterCounters z{};
+        z.bad_min = 0xffffffffu;
+        *a.ctr_next = z;
+    }
+    if (stop_after(a.stop_if)) return;
     unsigned long long g = 0, pcount = 0;
     unsigned int changed = 0, inv = 0, bad = 0xffffffffu;
     // U vertices per thread per step, every load of the step issued before
@@ -654,11 +675,6 @@ vertex_kernel(const VertexArgs<P, W> a) {
                 a.st_next[lv] = 0;
             }
         }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        IterCounters z{};
-        z.bad_min = 0xffffffffu;
-        *a.ctr_next = z;
     }
     // block reduction, one atomic per counter per block
 #pragma unroll
