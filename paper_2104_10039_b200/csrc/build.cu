@@ -378,6 +378,7 @@ __global__ void superstep_invalid_kernel(uint32_t nloc, uint32_t v_begin,
                                          const uint8_t* __restrict__ st_next,
                                          const uint64_t* __restrict__ s_off,
                                          IterCounters* __restrict__ ctr) {
+    if (!__ldg(&ctr->any_invalid)) return;  // the common case: nothing to rescan
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nloc; v += gridDim.x * blockDim.x) {
         if ((st_next[v] & kStInvalid) && ((st_cur[v] & kStActive) || s_off[v + 1] > s_off[v]))
             atomicMin(&ctr->bad_min, v_begin + v);

@@ -384,14 +384,10 @@ struct Engine {
             if (super) {  // new flag set -> new sparsified CSC (engine.hpp:207-214)
                 kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, timing ? e4 : nullptr,
                                       timing ? e5 : nullptr, &launches);
-                GGB_CUDA(cudaMemcpyAsync(h_ring, ctr, sizeof(IterCounters), cudaMemcpyDeviceToHost,
-                                         g.stream));
-                GGB_CUDA(cudaStreamSynchronize(g.stream));
-                if (timing) rb_ms = event_ms(e4, e5);
-                if (h_ring->any_invalid) {
-                    launch_superstep_invalid(g, st[cu], st[cu ^ 1], s_off, ctr);
-                    ++launches;
-                }
+                // bad-vertex rescan against the kept counts; exits at once on
+                // the device unless the vertex kernel saw an invalid property
+                launch_superstep_invalid(g, st[cu], st[cu ^ 1], s_off, ctr);
+                ++launches;
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
                 if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
@@ -405,6 +401,7 @@ struct Engine {
             GGB_CUDA(cudaStreamSynchronize(g.stream));
             const double batch_wall =
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (timing && super) rb_ms = event_ms(e4, e5);
             for (int k = 0; k < B; ++k) {
                 const uint64_t u = t + k;
                 const IterCounters& hc = h_ring[u % kRing];
