@@ -16,6 +16,9 @@
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
+
+/* largest property (bytes) the run loops keep on the stack: BP up to 32 states */
+#define OG_MAX_PSIZE 256
 #endif
 
 /* engine.cpp:9-14 (and graph.cpp:22-27, test_support.hpp:12-17) */
@@ -613,7 +616,7 @@ static int make_prog(int which, const og_params* p, uint64_t n, int* counter, pr
             out->psize = 4; out->init = wcc_init; out->identity = wcc_id; out->gather = wcc_gather;
             out->apply = wcc_apply; out->vstatus = wcc_vstatus; out->valid = wcc_valid; break;
         case OG_BP:
-            if (p->states < 2) return -1;
+            if (p->states < 2 || 8 * (size_t)p->states > OG_MAX_PSIZE) return -1;
             out->psize = 8 * (size_t)p->states; out->init = bp_init; out->identity = bp_id;
             out->gather = bp_gather; out->apply = bp_apply; out->vstatus = bp_vstatus;
             out->valid = bp_valid; break;
@@ -665,7 +668,7 @@ int og_run(const og_graph* g, int which, const og_params* params,
     uint8_t* status = (uint8_t*)xmalloc(n);
     uint8_t* status_next = (uint8_t*)xcalloc(n, 1);
     memset(status, 1, n);
-    uint8_t acc[64], fresh[64];
+    uint8_t acc[OG_MAX_PSIZE], fresh[OG_MAX_PSIZE];
 
     for (uint64_t t = 1; t <= cfg->max_iterations; ++t) {          /* :177 */
         const int mode = og_mode_for(cfg->scheme, t, cfg->alpha);
@@ -757,7 +760,7 @@ int og_step_range(const og_graph* g, int which, const og_params* params, int mod
     const uint8_t* prev = (const uint8_t*)prev_v;
     uint8_t* next = (uint8_t*)next_v;
     const int approx = mode == OG_MODE_APPROXIMATE, superstep = mode == OG_MODE_SUPERSTEP;
-    uint8_t acc[64], fresh[64];
+    uint8_t acc[OG_MAX_PSIZE], fresh[OG_MAX_PSIZE];
     uint64_t gathered = 0, processed = 0, changed = 0;
     int any_bad = 0;
     for (uint64_t v = v_begin; v < v_end; ++v) {

@@ -505,7 +505,17 @@ gg_status gg_run_bp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_bp_pa
                       Engine<BeliefProp<3>, void>::run(g, b, io); break; }
             case 4: { BeliefProp<4> b; b.coupling = p->coupling; b.epsilon = p->epsilon;
                       Engine<BeliefProp<4>, void>::run(g, b, io); break; }
-            default: throw Error(GG_INVALID_ARGUMENT, "bp states must be in [2,4] on device");
+            default: {
+                if (p->states < 2) throw Error(GG_INVALID_ARGUMENT, "bp states must be >= 2");
+                if (p->states > kBpMaxStates)
+                    throw Error(GG_INVALID_ARGUMENT, "bp states must be <= 16 on device");
+                BeliefPropDyn b;
+                b.states = p->states;
+                b.coupling = p->coupling;
+                b.epsilon = p->epsilon;
+                Engine<BeliefPropDyn, void>::run(g, b, io);
+                break;
+            }
         }
     });
 }

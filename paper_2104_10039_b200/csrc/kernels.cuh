@@ -377,7 +377,8 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     // Heavy programs fold the run in a rolled loop (one inlined gather);
     // without a second pass over the messages they shift the run through
     // registers (element 0 each step) instead of indexing a local array.
-    constexpr bool kShift = fold_unroll<P>() == 1 && MODE != kEdgeSuper && !PASS2;
+    constexpr bool kShift = fold_unroll<P>() == 1 && MODE != kEdgeSuper && !PASS2 &&
+                            sizeof(Message) <= 16;  // larger runs stay in local memory
     if constexpr (kShift) {
         if constexpr (MODE == kEdgeFoldStash) stash_rows<P, W>(a, xs, lane, t, m);  // before the shifts
 #pragma unroll 1

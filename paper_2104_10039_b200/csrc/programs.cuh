@@ -284,6 +284,96 @@ struct BeliefProp {
     __device__ double to_double(const Property& p, int i) const { return p.x[i]; }
 };
 
+// BeliefPropagationProgram with any state count 5..kBpMaxStates chosen at run
+// time (BeliefProp<S> covers 2..4 with compile-time loops); storage is a
+// fixed Belief<kBpMaxStates>, states >= S are never touched. Same formulas
+// and operation order as BeliefProp<S> (algorithms.cpp:9-69).
+constexpr int kBpMaxStates = 16;
+struct BeliefPropDyn {
+    using Property = Belief<kBpMaxStates>;
+    using Message = Property;
+    using Accum = Property;
+    static constexpr bool kMsgIsProp = true;
+    static constexpr bool kNeedsDegree = false;
+    static constexpr bool kHeavyGather = true;
+    int states = 5;
+    double coupling = 0.8, epsilon = 1e-6;
+
+    __device__ Property prior(uint32_t v) const {  // algorithms.cpp:9-23
+        Property p;
+        double sum = 0.0;
+        for (int i = 0; i < states; ++i) {
+            const uint64_t h = mix64((uint64_t)v * (uint64_t)states + (uint64_t)i);
+            p.x[i] = 1.0 + (double)(h >> 11) * 0x1.0p-53;
+            sum += p.x[i];
+        }
+        for (int i = 0; i < states; ++i) p.x[i] /= sum;
+        return p;
+    }
+    __device__ Property init_property(uint32_t v, uint64_t) const { return prior(v); }
+    __device__ Accum gather_identity() const {
+        Accum a;
+        for (int i = 0; i < states; ++i) a.x[i] = 1.0;
+        return a;
+    }
+    __device__ Message message(const Property& p, uint32_t) const { return p; }
+    __device__ double gather(Accum& acc, const Message& src, double) const {  // :25-48
+        const double off = (1.0 - coupling) / (double)(states - 1);
+        double src_sum = 0.0;
+        for (int i = 0; i < states; ++i) src_sum += src.x[i];
+        double l1_after = 0.0, l1_diff = 0.0, acc_sum = 0.0;
+        for (int i = 0; i < states; ++i) {
+            const double si = src.x[i];
+            const double msg = off * (src_sum - si) + coupling * si;
+            const double updated = acc.x[i] * msg;
+            l1_after += fabs(updated);
+            l1_diff += fabs(acc.x[i] - updated);
+            acc.x[i] = updated;
+            acc_sum += updated;
+        }
+        if (acc_sum > 0.0)
+            for (int i = 0; i < states; ++i) acc.x[i] /= acc_sum;
+        if (l1_after <= 0.0) return 0.0;
+        const double r = l1_diff / l1_after;
+        return r < 1.0 ? r : 1.0;
+    }
+    __device__ bool is_identity(const Accum& a) const {
+        for (int i = 0; i < states; ++i)
+            if (a.x[i] != 1.0) return false;
+        return true;
+    }
+    __device__ Accum combine(const Accum& a, const Accum& b) const {
+        if (is_identity(a)) return b;
+        if (is_identity(b)) return a;
+        Accum r;
+        double s = 0.0;
+        for (int i = 0; i < states; ++i) { r.x[i] = a.x[i] * b.x[i]; s += r.x[i]; }
+        if (s > 0.0)
+            for (int i = 0; i < states; ++i) r.x[i] /= s;
+        return r;
+    }
+    __device__ Property apply(uint32_t v, const Accum& acc, const Property&, uint64_t) const {
+        Property out = prior(v);  // algorithms.cpp:50-62
+        double sum = 0.0;
+        for (int i = 0; i < states; ++i) { out.x[i] *= acc.x[i]; sum += out.x[i]; }
+        if (sum > 0.0)
+            for (int i = 0; i < states; ++i) out.x[i] /= sum;
+        return out;
+    }
+    __device__ bool vstatus(const Property& b, const Property& a) const {  // :64-69
+        double l1 = 0.0;
+        for (int i = 0; i < states; ++i) l1 += fabs(b.x[i] - a.x[i]);
+        return l1 > epsilon;
+    }
+    __device__ bool estatus(double infl, double theta) const { return infl > theta; }
+    __device__ bool valid(const Property& p) const {
+        for (int i = 0; i < states; ++i)
+            if (!isfinite(p.x[i])) return false;
+        return true;
+    }
+    __device__ double to_double(const Property& p, int i) const { return p.x[i]; }
+};
+
 // BASELINE C4 BP: reference formulas, S = 2, coupling = the edge's fp32 c_e,
 // prior from an fp32 table, beliefs STORED as fp32 (arithmetic in f64).
 struct BeliefPropEdge {

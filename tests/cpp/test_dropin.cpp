@@ -170,6 +170,7 @@ int main() {
 
     all_schemes("bp2/power_law", pl, d_pl, gg::bp_spec(2, 0.8, 1e-6), 0.01, 1e-6, 30);
     all_schemes("bp3/power_law", pl, d_pl, gg::bp_spec(3, 0.7, 1e-6), 0.01, 1e-6, 30);
+    all_schemes("bp6/power_law", pl, d_pl, gg::bp_spec(6, 0.6, 1e-6), 0.01, 1e-6, 30);
 
     // The reference signature (graph uploaded inside the call).
     {

@@ -155,6 +155,20 @@ def test_random_graphs_all_programs(ggb, scheme, seed):
     assert total == 0
 
 
+@pytest.mark.parametrize("states", [4, 5, 8, 16])
+def test_bp_many_states(ggb, states):
+    """BeliefProp<S> for S <= 4, the run-time-S program above (any S up to
+    16), against the oracle's reference BP (algorithms.cpp:9-69)."""
+    g = Oracle.power_law(400, 6.0, 2.1, states)
+    for scheme in SCHEMES:
+        _, _, mism = compare(ggb, g, BP, scheme=scheme, sigma=0.5, theta=0.01, alpha=3,
+                             max_iterations=25, seed=states, states=states, coupling=0.6)
+        assert mism == 0
+    with pytest.raises(ValueError, match="<= 16"):
+        ggb.run(to_graph(ggb, g), ggb.BeliefPropagationProgram(17, 0.6, 1e-6),
+                ggb.EngineConfig(max_iterations=2))
+
+
 @pytest.mark.parametrize("seed", [1, 2])
 def test_edge_bp_fp32(ggb, seed):
     g = Oracle.power_law(600, 8.0, 2.1, seed)
