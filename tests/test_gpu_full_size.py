@@ -39,6 +39,12 @@ def _run_both(ggb, name, max_iterations, want_flags=False):
     cfg = ggb.EngineConfig("gg", bench.SIGMA, wl["theta"], bench.ALPHA, max_iterations,
                            wl["seed"])
     rep = ggb.run(dg, program, cfg, want_flags=want_flags)
+    # run-to-run determinism at full scale: a second run is bit-identical
+    again = ggb.run(dg, program, cfg)
+    assert np.array_equal(np.asarray(again.final_properties).view(np.uint8),
+                          np.asarray(rep.final_properties).view(np.uint8))
+    assert [r.processed_edges for r in again.per_iteration] == \
+        [r.processed_edges for r in rep.per_iteration]
     host = dg.to_host()
     dg.close()
     g = bench.ref_inputs(wl, host)
