@@ -107,6 +107,35 @@ __device__ __forceinline__ T shfl_idx_any(T v, int lane) {
     return out;
 }
 
+// Inter-warp hand-over within one kernel (the superstep carry chain): a value
+// is written with plain stores, then published by a release store of its
+// state word; readers acquire the state and read the value from L2.
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T ld_l2(const T* p) {
+    T out;
+    if constexpr (sizeof(T) % 8 == 0) {
+        const unsigned long long* s = reinterpret_cast<const unsigned long long*>(p);
+        unsigned long long* d = reinterpret_cast<unsigned long long*>(&out);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(T) / 8); ++i) d[i] = __ldcg(s + i);
+    } else {
+        static_assert(sizeof(T) % 4 == 0, "32-bit granular types only");
+        const unsigned int* s = reinterpret_cast<const unsigned int*>(p);
+        unsigned int* d = reinterpret_cast<unsigned int*>(&out);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(T) / 4); ++i) d[i] = __ldcg(s + i);
+    }
+    return out;
+}
+
 // L2 eviction policies (createpolicy) for the two access streams of the
 // gather: edge arrays are read once per iteration (evict_first), the
 // per-vertex message array is re-read randomly (evict_last).

@@ -111,6 +111,18 @@ struct Engine {
         }();
         return b;
     }
+    // Superstep scheme (GGB_SUPERSTEP): "chain" (default: one pass, carries
+    // from the in-kernel chain), "stash" (fold + stash, influence pass), or
+    // "pass2" (in-kernel influence + re-gathering pass 2).
+    static int superstep_scheme() {
+        static int s = [] {
+            const char* e = std::getenv("GGB_SUPERSTEP");
+            if (e && !std::strcmp(e, "stash")) return 1;
+            if (e && !std::strcmp(e, "pass2")) return 2;
+            return 0;
+        }();
+        return s;
+    }
     static int grid_stash(DevGraph& g) {
         static int cached = 0;
         if (!cached) cached = occupancy_grid((const void*)edge_influence_kernel<P, W>,
@@ -206,7 +218,13 @@ struct Engine {
         Acc* lane_pre = nullptr;
         uint32_t* task_info = nullptr;
         uint32_t* run_meta = nullptr;
-        if (cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) {
+        const int sscheme = superstep_scheme();
+        // chain scheme: per-task slots + the task ticket, cleared per superstep
+        constexpr size_t kSlot = chain_packed<Acc>() ? sizeof(ulonglong2) : sizeof(uint32_t);
+        char* chain = nullptr;
+        if ((cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) && sscheme == 0)
+            chain = static_cast<char*>(ws.get("chain", ntask_cap * kSlot + 16));
+        if ((cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) && sscheme == 1) {
             const size_t sbytes = (g.full.ntasks * kChunkEdges + kRun) * sizeof(Msg);
             const size_t pbytes = (g.full.nruns + 1) * sizeof(Acc);
             const bool have = ws.bufs.count("stash") && ws.bufs["stash"].bytes >= sbytes;
@@ -325,6 +343,11 @@ struct Engine {
             ea.lane_pre = lane_pre;
             ea.run_meta = run_meta;
             ea.task_info = task_info;
+            if (chain) {
+                ea.cdesc = reinterpret_cast<ulonglong2*>(chain);
+                ea.chain = reinterpret_cast<uint32_t*>(chain);
+                ea.ticket = reinterpret_cast<uint32_t*>(chain + L.ntasks * kSlot);
+            }
             ea.bitmap = bitmap;
             ea.theta = cfg.theta;
             ea.stop_if = k ? ring + (u - 1) % kRing : nullptr;
@@ -357,7 +380,10 @@ struct Engine {
                 // every edge of the sparsified list (and of the full list under
                 // the accurate scheme) belongs to a processed vertex
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
-                if (super && stash) launch_edge<kEdgeFoldStash>(g, ea);
+                if (super && chain) {
+                    GGB_CUDA(cudaMemsetAsync(chain, 0, L.ntasks * kSlot + 4, g.stream));
+                    launch_edge<kEdgeChain>(g, ea);
+                } else if (super && stash) launch_edge<kEdgeFoldStash>(g, ea);
                 else if (super) launch_edge<kEdgeSuper>(g, ea);
                 else if (all_proc && nhot) {
                     if constexpr (kHotOK) launch_edge_hot(g, ea, nhot);
@@ -367,12 +393,16 @@ struct Engine {
                 ++launches;
             }
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 1), g.stream));
-            if (super) vertex_kernel<P, W, true><<<grid1d(nloc), 256, 0, g.stream>>>(va);
-            else vertex_kernel<P, W, false><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            if (super && chain)
+                vertex_kernel<P, W, kVtxChain><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            else if (super)
+                vertex_kernel<P, W, kVtxCarry><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            else
+                vertex_kernel<P, W, kVtxPlain><<<grid1d(nloc), 256, 0, g.stream>>>(va);
             GGB_CUDA(cudaGetLastError());
             ++launches;
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 2), g.stream));
-            if (super && L.ntasks) {  // flags of vertices whose fold began in an earlier task
+            if (super && L.ntasks && !chain) {  // flags of vertices whose fold began in an earlier task
                 if (stash)
                     edge_influence_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
                 else

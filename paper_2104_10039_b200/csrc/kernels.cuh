@@ -82,7 +82,13 @@ enum : int {
     kEdgeFoldStash = 3,  // superstep pass 1 of the stash scheme: fold + hand every
                          // run's messages, prefix and vertex marks to the
                          // influence pass (edge_influence_kernel)
+    kEdgeChain = 4,  // superstep in one pass: fold + influence / estatus, the carry
+                     // into a task's continuing vertex from the chain (chain_carry)
 };
+
+// chain states (EdgeArgs::chain), per task, for the vertex continuing past it
+constexpr uint32_t kChainPiece = 1;  // hv[t] holds the task's whole piece
+constexpr uint32_t kChainIncl = 2;   // tv[t] holds its inclusive fold (from the vertex start)
 
 // non-empty vertex starts of one task, relative to the task start, clamped
 // to [-1, 513] (-1: began in an earlier task, 513: ends in a later one)
@@ -121,6 +127,11 @@ struct EdgeArgs {
     typename P::Accum* __restrict__ lane_pre;
     uint32_t* __restrict__ run_meta;
     uint32_t* __restrict__ task_info;  // [task] kTaskCont | end of the first vertex
+    // kEdgeChain: per task {state, value} (16-byte slots, accumulators of <= 8
+    // bytes) or the state alone (values in hv / tv), and the task ticket
+    ulonglong2* __restrict__ cdesc;
+    uint32_t* __restrict__ chain;
+    uint32_t* __restrict__ ticket;
     uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
     double theta;
     const IterCounters* stop_if;            // batched iterations: the previous iteration's counters
@@ -242,22 +253,32 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
 // end of the task's first vertex, clamped to 513)
 constexpr uint32_t kTaskCont = 1u << 16;  // the first vertex began in an earlier task
 
-// Rewrite the flags this lane owns (bits of `own`, relative to P0) to
-// `kbits`; flags of edges of skipped vertices persist (engine.hpp:204-211).
-__device__ __forceinline__ void write_flags(uint32_t* __restrict__ bitmap, uint64_t pad,
-                                            uint64_t P0, uint64_t lo, uint32_t own,
-                                            uint32_t kbits) {
-    if (!own) return;
-    const uint64_t e0 = lo - pad;  // local edge id of bit (lo - P0)
-    const uint32_t shift_in = (uint32_t)(lo - P0);
-    const uint32_t O = own >> shift_in, K = kbits >> shift_in;
-    const uint32_t sh = (uint32_t)(e0 & 31);
-    const uint64_t K64 = (uint64_t)K << sh, O64 = (uint64_t)O << sh;
-    uint32_t* wp = bitmap + (e0 >> 5);
-    if ((uint32_t)O64) { atomicAnd(wp, ~(uint32_t)O64); atomicOr(wp, (uint32_t)K64); }
-    if ((uint32_t)(O64 >> 32)) {
-        atomicAnd(wp + 1, ~(uint32_t)(O64 >> 32));
-        atomicOr(wp + 1, (uint32_t)(K64 >> 32));
+// Rewrite the flags of a task's processed edges (lane bits `own`, relative
+// to its run) to `kbits`; flags of edges of skipped vertices persist
+// (engine.hpp:204-211). Warp-collective: the lanes' 16-bit fields are
+// reassembled into bitmap words (word k of the task starts at task position
+// 32k - q); a word that lies inside the task belongs to this warp alone and
+// is stored (read-modify-write only where some of its flags persist), the
+// two words shared with the neighbouring tasks take atomics.
+__device__ __forceinline__ void warp_write_flags(uint32_t* __restrict__ bitmap, uint64_t pad,
+                                                 uint64_t tstart, uint32_t own, uint32_t kbits,
+                                                 int lane) {
+    const int64_t b = (int64_t)tstart - (int64_t)pad;  // local edge id of task position 0
+    const int64_t w0 = b >> 5;                          // floor
+    const int q = (int)(b - (w0 << 5));
+    const int s = 32 * lane - q;  // first task position of word w0 + lane
+    const int l = s >> 4, off = s & 15;
+    auto get = [&](uint32_t v, int src) -> uint64_t {
+        const uint32_t x = __shfl_sync(0xffffffffu, v, src & 31);
+        return (src >= 0 && src < kWarp) ? (uint64_t)(x & 0xffffu) : 0ull;
+    };
+    const uint64_t O = get(own, l) | get(own, l + 1) << 16 | get(own, l + 2) << 32;
+    const uint64_t K = get(kbits, l) | get(kbits, l + 1) << 16 | get(kbits, l + 2) << 32;
+    const uint32_t o = (uint32_t)(O >> off), k = (uint32_t)(K >> off);
+    if (lane <= 16 && o) {
+        uint32_t* wp = bitmap + (w0 + lane);
+        if (s >= 0 && s + 32 <= kChunkEdges) *wp = o == 0xffffffffu ? k : ((*wp & ~o) | k);
+        else { atomicAnd(wp, ~o); atomicOr(wp, k); }
     }
 }
 
@@ -279,6 +300,96 @@ __device__ __forceinline__ void stash_rows(const EdgeArgs<P, W>& a, char* xs, in
     }
 }
 
+// The carry into task t's first vertex (which began in an earlier task t0):
+// tv[t0] (+) hv[t0+1] (+) ... (+) hv[t-1], folded left to right -- the value
+// the vertex kernel's task-order join produces. Every task a vertex continues
+// past publishes its piece (kChainPiece) as soon as its fold is done and, once
+// it has its own carry, the inclusive fold (kChainIncl; the vertex's first
+// task publishes its tail piece as inclusive at once). The warp looks back
+// from t-1 for the nearest inclusive value and folds the pieces after it in
+// order; any inclusive value it meets is itself that same left-to-right fold,
+// so the result does not depend on timing. Tasks are claimed in order
+// (ticket), so every task looked at is held by a running warp that never
+// waits on a later task: the look-back always completes.
+//
+// Accumulators of <= 8 bytes travel with their state in one 16-byte slot
+// (one relaxed vector store / load, no fence); larger ones are written to
+// hv / tv and published by a release store of the state.
+template <class Accum>
+__host__ __device__ constexpr bool chain_packed() { return sizeof(Accum) <= 8; }
+
+template <class Accum>
+__device__ __forceinline__ void chain_put(ulonglong2* d, uint32_t state, const Accum& v) {
+    unsigned long long bits = 0;
+    memcpy(&bits, &v, sizeof(Accum));
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};"
+                 :: "l"(d), "l"((unsigned long long)state), "l"(bits) : "memory");
+}
+template <class Accum>
+__device__ __forceinline__ uint32_t chain_get(const ulonglong2* d, Accum& v) {
+    unsigned long long st, bits;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(st), "=l"(bits) : "l"(d) : "memory");
+    memcpy(&v, &bits, sizeof(Accum));
+    return (uint32_t)st;
+}
+
+template <class P, class W>
+__device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a, uint64_t t, int lane) {
+    using Accum = typename P::Accum;
+    constexpr bool kPacked = chain_packed<Accum>();
+    int64_t base = (int64_t)t - 1;  // newest task of the window; lane i looks at base - i
+    Accum v = a.prog.gather_identity();
+    int L;
+    for (;;) {
+        const int64_t j = base - lane;
+        uint32_t s = kChainIncl;
+        if (j >= 0) {
+            if constexpr (kPacked) s = chain_get(a.cdesc + j, v);
+            else s = ld_acquire(a.chain + j);
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, s == kChainIncl);
+        const uint32_t none = __ballot_sync(0xffffffffu, s == 0);
+        if (incl) {
+            L = __ffs(incl) - 1;
+            if ((none & ((1u << L) - 1u)) == 0) break;
+        } else if (!none) {
+            base -= kWarp;  // 32 pieces, no inclusive value yet: look further back
+            continue;
+        }
+        __nanosleep(64);  // a piece in between is still being folded
+    }
+    if constexpr (!kPacked) {  // values from L2 after the acquire
+        __syncwarp();
+        const int64_t j = base - lane;
+        if (lane <= L) v = lane == L ? ld_l2(a.tv + j) : ld_l2(a.hv + j);
+    }
+    // inclusive value at lane L, pieces at lanes L-1 .. 0 (ascending tasks)
+    Accum acc = shfl_idx_any(v, L);
+    for (int i = L - 1; i >= 0; --i) acc = a.prog.combine(acc, shfl_idx_any(v, i));
+    // later windows (all published when they were passed over); an inclusive
+    // value met there equals the fold so far, so it replaces it exactly
+    for (int64_t wb = base + kWarp; wb <= (int64_t)t - 1; wb += kWarp) {
+        const int64_t j = wb - lane;
+        uint32_t s;
+        if constexpr (kPacked) {
+            s = chain_get(a.cdesc + j, v);
+        } else {
+            s = ld_acquire(a.chain + j);
+            __syncwarp();
+            v = s == kChainIncl ? ld_l2(a.tv + j) : ld_l2(a.hv + j);
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, s == kChainIncl);
+        int start = kWarp - 1;
+        if (incl) {
+            const int L2 = __ffs(incl) - 1;
+            acc = shfl_idx_any(v, L2);
+            start = L2 - 1;
+        }
+        for (int i = start; i >= 0; --i) acc = a.prog.combine(acc, shfl_idx_any(v, i));
+    }
+    return acc;
+}
+
 template <class P, class W, int MODE, bool PASS2, bool HOT = false>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, char* xs,
                                           uint64_t t, int lane, uint64_t pol_stream,
@@ -286,6 +397,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     using Accum = typename P::Accum;
     using Message = typename P::Message;
     constexpr bool SUPER = MODE == kEdgeSuper;
+    constexpr bool CHAIN = MODE == kEdgeChain;
     const uint64_t tstart = t * kChunkEdges;
     const uint64_t r = t * kWarp + lane;
     const uint64_t P0 = r * kRun;
@@ -347,6 +459,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     bool pk = true;
     if constexpr (MODE != kEdgePlain)
         if (len > 0) pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
+    const bool pk_first = pk;  // lane 0: the task's first vertex
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
     uint32_t bmask = 0;  // positions where a later vertex of the run starts
     Accum x = a.prog.gather_identity(), hvv = x;
@@ -377,7 +490,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     // Heavy programs fold the run in a rolled loop (one inlined gather);
     // without a second pass over the messages they shift the run through
     // registers (element 0 each step) instead of indexing a local array.
-    constexpr bool kShift = fold_unroll<P>() == 1 && MODE != kEdgeSuper && !PASS2 &&
+    constexpr bool kShift = fold_unroll<P>() == 1 && !SUPER && !CHAIN && !PASS2 &&
                             sizeof(Message) <= 16;  // larger runs stay in local memory
     if constexpr (kShift) {
         if constexpr (MODE == kEdgeFoldStash) stash_rows<P, W>(a, xs, lane, t, m);  // before the shifts
@@ -418,19 +531,59 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             const bool cont_after = nb > rhi;  // the vertex goes on past this task
             const bool first_cont = cont && tk == 0;
             if (first_cont) a.hv[t] = S;
-            if (cont_after) a.tv[t] = S;
-            else if (!first_cont) a.acc_out[a.nz_vid[i0 + tk]] = S;
+            if (cont_after && !(CHAIN && first_cont)) a.tv[t] = S;
+            else if (!cont_after && !first_cont) a.acc_out[a.nz_vid[i0 + tk]] = S;
+            if (CHAIN && cont_after) {  // publish for the tasks this vertex continues into
+                const uint32_t state = first_cont ? kChainPiece : kChainIncl;
+                if constexpr (chain_packed<Accum>()) {
+                    chain_put(a.cdesc + t, state, S);
+                } else {
+                    __threadfence();
+                    st_release(a.chain + t, state);
+                }
+            }
         }
     }
-    if constexpr (SUPER) {
+    Accum carry_in = a.prog.gather_identity();
+    // the vertex spans the task: lane 31 (which published the piece S)
+    // publishes the inclusive fold once the carry is known
+    auto publish_incl = [&](const Accum& carry) {
+        if (st0[1] > kChunkEdges && lane == kWarp - 1) {
+            const Accum inc = a.prog.combine(carry, S);
+            a.tv[t] = inc;
+            if constexpr (chain_packed<Accum>()) {
+                chain_put(a.cdesc + t, kChainIncl, inc);
+            } else {
+                __threadfence();
+                st_release(a.chain + t, kChainIncl);
+            }
+        }
+    };
+    if constexpr (CHAIN) {
+        if (cont) {  // warp-uniform
+            // the carry of a vertex the skip test leaves out is never read:
+            // its chain is closed at once (no look-back). The look-back comes
+            // right after the fold: the chain advances at the rate tasks
+            // publish inclusive values (measured: any later point is slower).
+            if (__shfl_sync(0xffffffffu, pk_first, 0)) carry_in = chain_carry(a, t, lane);
+            publish_incl(carry_in);
+        }
+    }
+    if constexpr (SUPER || CHAIN) {
         // influence of each edge against its exclusive running prefix
         // (engine.hpp:204-211); a vertex whose fold began in an earlier task
-        // is handled by pass 2 with that task's carry.
+        // is handled by pass 2 with that task's carry (kEdgeSuper) or after
+        // the chain look-back (kEdgeChain).
         Accum run = a.prog.gather_identity();
         bool skip_head = false;
         if (cont && hk == 0) {
-            if (PASS2) run = a.carry[t];
-            else skip_head = true;
+            if (CHAIN) {
+                run = carry_in;
+            } else if (PASS2) {
+                run = a.carry[t];
+            } else {
+                skip_head = true;
+            }
         } else if (PASS2) {
             skip_head = true;  // pass 2 only rewrites the continuing vertex
         }
@@ -457,7 +610,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 }
             }
         });
-        write_flags(a.bitmap, a.pad, P0, lo, own, kbits);
+        warp_write_flags(a.bitmap, a.pad, tstart, own, kbits, lane);
     }
     if constexpr (MODE == kEdgeFoldStash) {
         if (lane == 0) a.task_info[t] = cont ? (kTaskCont | (uint32_t)st0[1]) : 0u;
@@ -479,6 +632,17 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
     const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
+    if constexpr (MODE == kEdgeChain) {  // tasks claimed in order (see chain_carry)
+        for (;;) {
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(a.ticket, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= a.ntasks) break;
+            edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], xs_all[threadIdx.x >> 5], t,
+                                         lane, pol_stream, pol_hot, pol_cold);
+        }
+        return;
+    }
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
@@ -570,29 +734,35 @@ edge_influence_kernel(const EdgeArgs<P, W> a) {
                 for (int j = 0; j < kRun; ++j) mm[j] = a.stash[P0 + j];
             }
         }
-        if (!own) continue;
-        const bool head = (info & kTaskCont) && P0 < t * kChunkEdges + (info & 0xffffu);
-        Accum run = a.prog.combine(head ? a.carry[t] : a.prog.gather_identity(), a.lane_pre[r]);
         uint32_t kbits = 0;
-        for_run<P>([&](int j) {
-            if ((meta >> j) & 1u) run = a.prog.gather_identity();
-            if ((own >> j) & 1u) {
-                double w = 1.0;
-                if constexpr (!std::is_void_v<W>) w = (double)a.w[P0 + j];
-                const double infl = a.prog.gather(run, mm[j], w);
-                if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
-            }
-        });
-        write_flags(a.bitmap, a.pad, P0, P0 > a.pad ? P0 : a.pad, own, kbits);
+        if (own) {
+            const bool head = (info & kTaskCont) && P0 < t * kChunkEdges + (info & 0xffffu);
+            Accum run = a.prog.combine(head ? a.carry[t] : a.prog.gather_identity(), a.lane_pre[r]);
+            for_run<P>([&](int j) {
+                if ((meta >> j) & 1u) run = a.prog.gather_identity();
+                if ((own >> j) & 1u) {
+                    double w = 1.0;
+                    if constexpr (!std::is_void_v<W>) w = (double)a.w[P0 + j];
+                    const double infl = a.prog.gather(run, mm[j], w);
+                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
+                }
+            });
+        }
+        warp_write_flags(a.bitmap, a.pad, t * kChunkEdges, own, kbits, lane);
     }
 }
 
 // Vertex epilogue: the accumulator of vertex v is acc_out[v] when its list
 // lies inside one task, else tv[t0] (+) hv[t0+1] (+) ... (+) hv[t1] in task
 // order; then GG-Apply, GG-VStatus, valid, message, status, counters.
-template <class P, class W, bool SUPER>
+// VK: kVtxPlain, kVtxCarry (superstep, stash / pass-2 schemes: also writes
+// carry[t]), kVtxChain (superstep, chain scheme: tv[t1-1] already holds the
+// left-to-right fold up to task t1-1, so the join is one combine).
+enum : int { kVtxPlain = 0, kVtxCarry = 1, kVtxChain = 2 };
+template <class P, class W, int VK>
 __global__ void __launch_bounds__(256)
 vertex_kernel(const VertexArgs<P, W> a) {
+    constexpr bool SUPER = VK != kVtxPlain;
     using Accum = typename P::Accum;
     using Property = typename P::Property;
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next iteration's counters, even if skipped
@@ -644,10 +814,12 @@ vertex_kernel(const VertexArgs<P, W> a) {
                                    t1 = (o1[i] - 1 + a.pad) / kChunkEdges;
                     if (t0 == t1) {
                         acc = acc1[i];
+                    } else if constexpr (VK == kVtxChain) {
+                        acc = a.prog.combine(a.tv[t1 - 1], a.hv[t1]);
                     } else {
                         acc = a.tv[t0];
                         for (uint64_t t = t0 + 1; t <= t1; ++t) {
-                            if constexpr (SUPER) a.carry[t] = acc;
+                            if constexpr (VK == kVtxCarry) a.carry[t] = acc;
                             acc = a.prog.combine(acc, a.hv[t]);
                         }
                     }
