@@ -48,20 +48,44 @@ static inline unsigned grid_for(uint64_t n, int block, uint64_t cap = 148ull * 6
 // --------------------------------------------------------------------------
 // engine.cpp:63-75: flag(e) = (mix64(key ^ e) >> 11) * 2^-53 < sigma.
 // The product is exact (a 53-bit integer times a power of two), so the test
-// is the integer compare (mix64(key ^ e) >> 11) < ceil(sigma * 2^53) = thr.
-// One thread per bitmap word (32 independent hashes in flight).
+// is the integer compare (mix64(key ^ e) >> 11) < ceil(sigma * 2^53) = thr,
+// i.e. mix64(key ^ e) < T = thr << 11 (thr < 2^53; sigma = 1 keeps all).
+// One thread per bitmap word (32 independent hashes in flight). The test
+// needs only the high word of the final mix: h_hi = x_hi ^ (x_hi >> 31) of
+// the last product x, whose high word is three 32-bit multiplies; the low
+// word is computed only when h_hi ties T's high word.
+__device__ __forceinline__ bool keep_edge(uint64_t x, uint64_t T) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    const uint64_t y = x ^ (x >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    constexpr uint32_t c_lo = 0x133111ebu, c_hi = 0x94d049bbu;  // 0x94d049bb133111eb
+    const uint32_t xhi = __umulhi(ylo, c_lo) + ylo * c_hi + yhi * c_lo;
+    const uint32_t hhi = xhi ^ (xhi >> 31);
+    const uint32_t Thi = (uint32_t)(T >> 32);
+    if (hhi != Thi) return hhi < Thi;
+    const uint64_t xf = y * 0x94d049bb133111ebull;  // tie on the high word (rare)
+    return (xf ^ (xf >> 31)) < T;
+}
+
 __global__ void sparsify_kernel(uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_loc,
-                                uint64_t e_base, uint64_t thr, uint64_t key) {
+                                uint64_t e_base, uint64_t T, uint64_t key, int keep_all) {
+    const bool aligned = (e_base & 31) == 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nwords;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t word = 0;
         if (i < nwords) {
             const uint64_t e0 = i * 32;
             const int nb = e_loc - e0 < 32 ? (int)(e_loc - e0) : 32;
+            if (keep_all) {
+                word = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+            } else if (nb == 32 && aligned) {  // key ^ (base | b) = (key ^ base) ^ b
+                const uint64_t k0 = key ^ (e_base + e0);
 #pragma unroll 8
-            for (int b = 0; b < 32; ++b) {
-                const bool f = b < nb && (mix64(key ^ (e_base + e0 + b)) >> 11) < thr;
-                word |= (f ? 1u : 0u) << b;
+                for (int b = 0; b < 32; ++b) word |= (keep_edge(k0 ^ (uint64_t)b, T) ? 1u : 0u) << b;
+            } else {
+                for (int b = 0; b < nb; ++b)
+                    word |= (keep_edge(key ^ (e_base + e0 + b), T) ? 1u : 0u) << b;
             }
         }
         bitmap[i] = word;  // bitmap[nwords] is the zero guard word
@@ -71,8 +95,9 @@ __global__ void sparsify_kernel(uint32_t* __restrict__ bitmap, uint64_t nwords, 
 void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
     const uint64_t thr = all_ones ? (1ull << 53) : (uint64_t)std::ceil(sigma * 0x1.0p53);
+    const int keep_all = thr >= (1ull << 53) ? 1 : 0;  // (h >> 11) < 2^53 always
     sparsify_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(
-        bitmap, nwords, g.e_loc, g.e_base, thr, mix64(seed));
+        bitmap, nwords, g.e_loc, g.e_base, keep_all ? 0 : thr << 11, mix64(seed), keep_all);
     GGB_CUDA(cudaGetLastError());
 }
 
