@@ -295,44 +295,6 @@ __device__ __forceinline__ M ld_msg2(const M* p, bool hot, uint64_t ph, uint64_t
     return out;
 }
 
-// ---- warp row transposes through shared memory ------------------------
-// A warp holds 32 rows of ROWB bytes (lane l: row l, in registers) that are
-// consecutive in global memory. Storing them lane-by-lane would make every
-// store instruction touch 32 lines; instead rows go to shared memory in
-// 16-byte chunks, XOR-swizzled by row (conflict-free both ways), and come
-// back out as chunk c = i*32 + lane, so each global access instruction
-// covers 512 contiguous bytes. xs: 32 * ROWB bytes of this warp's smem.
-template <int ROWB>
-struct WarpRows {
-    static constexpr int Q = ROWB / 16;  // chunks per row (power of two)
-    static_assert(ROWB % 16 == 0 && (Q & (Q - 1)) == 0, "row of 16-byte chunks");
-    __device__ static uint32_t at(int row, int q) { return row * ROWB + ((q ^ (row % Q)) * 16); }
-    // registers -> global (gdst: 32*ROWB bytes, 16-byte aligned)
-    __device__ static void store(char* xs, int lane, const uint4 (&row)[Q], uint4* gdst) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) *reinterpret_cast<uint4*>(xs + at(lane, q)) = row[q];
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            const int c = i * 32 + lane;
-            __stcs(gdst + c, *reinterpret_cast<const uint4*>(xs + at(c / Q, c % Q)));  // streaming: keep L2 for gathers
-        }
-        __syncwarp();
-    }
-    // global -> registers
-    __device__ static void load(char* xs, int lane, const uint4* gsrc, uint4 (&row)[Q]) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            const int c = i * 32 + lane;
-            *reinterpret_cast<uint4*>(xs + at(c / Q, c % Q)) = __ldcs(gsrc + c);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < Q; ++q) row[q] = *reinterpret_cast<const uint4*>(xs + at(lane, q));
-        __syncwarp();
-    }
-};
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

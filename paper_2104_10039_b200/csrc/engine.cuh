@@ -111,31 +111,6 @@ struct Engine {
         }();
         return b;
     }
-    // Superstep scheme (GGB_SUPERSTEP): "chain" (default: one pass, carries
-    // from the in-kernel chain), "stash" (fold + stash, influence pass), or
-    // "pass2" (in-kernel influence + re-gathering pass 2).
-    static int superstep_scheme() {
-        static int s = [] {
-            const char* e = std::getenv("GGB_SUPERSTEP");
-            if (e && !std::strcmp(e, "stash")) return 1;
-            if (e && !std::strcmp(e, "pass2")) return 2;
-            return 0;
-        }();
-        return s;
-    }
-    static int grid_stash(DevGraph& g) {
-        static int cached = 0;
-        if (!cached) cached = occupancy_grid((const void*)edge_influence_kernel<P, W>,
-                                             kBlockThreads, 0, g.num_sms);
-        return cached;
-    }
-    static int grid_pass2(DevGraph& g) {
-        static int cached = 0;
-        if (!cached) cached = occupancy_grid((const void*)edge_pass2_kernel<P, W>, kBlockThreads, 0,
-                                             g.num_sms);
-        return cached;
-    }
-
     // Algorithmic HBM bytes (SURVEY §8(d) byte formula B = E_p*b_e + N*b_v;
     // a superstep adds the bitmap write E_p/8).
     static uint64_t edge_bytes(uint64_t edges, bool super) {
@@ -210,41 +185,12 @@ struct Engine {
         const uint64_t ntask_cap = g.full.ntasks + 2;
         Acc* hv = ws.get<Acc>("hv", ntask_cap);
         Acc* tv = ws.get<Acc>("tv", ntask_cap);
-        Acc* carry = ws.get<Acc>("carry", ntask_cap);
-        // superstep stash (see EdgeArgs::stash): one message per padded
-        // position of the full list + one prefix per run, when HBM allows
-        // (else pass 2 re-gathers).
-        Msg* stash = nullptr;
-        Acc* lane_pre = nullptr;
-        uint32_t* task_info = nullptr;
-        uint32_t* run_meta = nullptr;
-        const int sscheme = superstep_scheme();
-        // chain scheme: per-task slots + the task ticket, cleared per superstep
+        // superstep chain (kEdgeChain): per-task slots + the task ticket,
+        // cleared before each superstep
         constexpr size_t kSlot = chain_packed<Acc>() ? sizeof(ulonglong2) : sizeof(uint32_t);
         char* chain = nullptr;
-        if ((cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) && sscheme == 0)
+        if (cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG)
             chain = static_cast<char*>(ws.get("chain", ntask_cap * kSlot + 16));
-        if ((cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG) && sscheme == 1) {
-            const size_t sbytes = (g.full.ntasks * kChunkEdges + kRun) * sizeof(Msg);
-            const size_t pbytes = (g.full.nruns + 1) * sizeof(Acc);
-            const bool have = ws.bufs.count("stash") && ws.bufs["stash"].bytes >= sbytes;
-            size_t free_b = 0, total_b = 0;
-            if (!have) {  // free device memory + what the stream-ordered pool holds unused
-                GGB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-                cudaMemPool_t pool;
-                uint64_t reserved = 0, used = 0;
-                GGB_CUDA(cudaDeviceGetDefaultMemPool(&pool, g.device));
-                GGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-                GGB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-                if (reserved > used) free_b += reserved - used;
-            }
-            if (have || free_b > sbytes + pbytes + (4ull << 30)) {
-                stash = static_cast<Msg*>(ws.get("stash", sbytes));
-                lane_pre = ws.get<Acc>("lane_pre", g.full.nruns + 1);
-                task_info = ws.get<uint32_t>("task_info", g.full.ntasks + 1);
-                run_meta = ws.get<uint32_t>("run_meta", g.full.nruns + 1);
-            }
-        }
         const uint64_t nwords = (g.e_loc + 31) / 32;
         const size_t wsz = (size_t)weight_bytes<W>();
         uint32_t* bitmap = nullptr;
@@ -338,11 +284,6 @@ struct Engine {
             ea.acc_out = acc_out;
             ea.hv = hv;
             ea.tv = tv;
-            ea.carry = carry;
-            ea.stash = super ? stash : nullptr;
-            ea.lane_pre = lane_pre;
-            ea.run_meta = run_meta;
-            ea.task_info = task_info;
             if (chain) {
                 ea.cdesc = reinterpret_cast<ulonglong2*>(chain);
                 ea.chain = reinterpret_cast<uint32_t*>(chain);
@@ -369,7 +310,6 @@ struct Engine {
             va.acc_out = acc_out;
             va.hv = hv;
             va.tv = tv;
-            va.carry = carry;
             IterCounters* ctr = ring + u % kRing;
             va.ctr = ctr;
             va.ctr_next = ring + (u + 1) % kRing;
@@ -380,12 +320,10 @@ struct Engine {
                 // every edge of the sparsified list (and of the full list under
                 // the accurate scheme) belongs to a processed vertex
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
-                if (super && chain) {
+                if (super) {
                     GGB_CUDA(cudaMemsetAsync(chain, 0, L.ntasks * kSlot + 4, g.stream));
                     launch_edge<kEdgeChain>(g, ea);
-                } else if (super && stash) launch_edge<kEdgeFoldStash>(g, ea);
-                else if (super) launch_edge<kEdgeSuper>(g, ea);
-                else if (all_proc && nhot) {
+                } else if (all_proc && nhot) {
                     if constexpr (kHotOK) launch_edge_hot(g, ea, nhot);
                 }
                 else if (all_proc) launch_edge<kEdgePlain>(g, ea);
@@ -393,24 +331,11 @@ struct Engine {
                 ++launches;
             }
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 1), g.stream));
-            if (super && chain)
-                vertex_kernel<P, W, kVtxChain><<<grid1d(nloc), 256, 0, g.stream>>>(va);
-            else if (super)
-                vertex_kernel<P, W, kVtxCarry><<<grid1d(nloc), 256, 0, g.stream>>>(va);
-            else
-                vertex_kernel<P, W, kVtxPlain><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            if (super) vertex_kernel<P, W, true><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            else vertex_kernel<P, W, false><<<grid1d(nloc), 256, 0, g.stream>>>(va);
             GGB_CUDA(cudaGetLastError());
             ++launches;
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 2), g.stream));
-            if (super && L.ntasks && !chain) {  // flags of vertices whose fold began in an earlier task
-                if (stash)
-                    edge_influence_kernel<P, W><<<grid_stash(g), kBlockThreads, 0, g.stream>>>(ea);
-                else
-                    edge_pass2_kernel<P, W><<<grid_pass2(g), kBlockThreads, 0, g.stream>>>(ea);
-                GGB_CUDA(cudaGetLastError());
-                ++launches;
-            }
-            if (timing) GGB_CUDA(cudaEventRecord(ev(k, 3), g.stream));
             if (super) {  // new flag set -> new sparsified CSC (engine.hpp:207-214)
                 kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, timing ? e4 : nullptr,
                                       timing ? e5 : nullptr, &launches);
@@ -460,7 +385,7 @@ struct Engine {
                     r.processed_edges = hc.gathered;
                     r.active_vertices = hc.processed;
                     r.wall_seconds = wall;
-                    r.edge_ms = timing ? event_ms(ev(k, 0), ev(k, 1)) + event_ms(ev(k, 2), ev(k, 3)) : 0.0;
+                    r.edge_ms = timing ? event_ms(ev(k, 0), ev(k, 1)) : 0.0;
                     r.vertex_ms = timing ? event_ms(ev(k, 1), ev(k, 2)) : 0.0;
                     r.kernel_ms = r.edge_ms + r.vertex_ms;
                     r.rebuild_ms = rb_ms;

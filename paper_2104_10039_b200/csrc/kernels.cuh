@@ -2,20 +2,15 @@
 //
 // Replaces the reference's iteration body (engine.hpp:177-241):
 //   edge_kernel    gather fold (GG-Gather, engine.hpp:198-213) over the
-//                  current list; in a superstep (kEdgeFoldStash) it also hands
-//                  every run's messages and prefixes to the influence pass;
+//                  current list; in a superstep (kEdgeChain) also the
+//                  influence + GG-EStatus of every processed edge into the
+//                  active-edge bitmap (engine.hpp:204-211), with the carry
+//                  into each task's continuing vertex from a look-back over
+//                  the other tasks' published pieces (chain_carry);
 //   edge_kernel_hot the approximate fold with the hottest message slots in
 //                  shared memory (4-byte messages);
 //   vertex_kernel  skip test (:196), GG-Apply / GG-VStatus / valid (:216-224),
-//                  next = prev carry-over (:183), iteration counters, and the
-//                  superstep carry into each task;
-//   edge_influence influence + GG-EStatus of every processed edge into the
-//                  active-edge bitmap (engine.hpp:204-211), streaming the
-//                  stash with the carried prefixes;
-//   kEdgeSuper + edge_pass2_kernel: the same superstep without the stash
-//                  (fallback when HBM cannot hold it): influences in the fold
-//                  kernel, re-gathering pass 2 for the vertices continuing
-//                  from an earlier task.
+//                  next = prev carry-over (:183), iteration counters.
 //
 // Layout (per rank): the list (full or sparsified CSC) is addressed by PADDED
 // positions P = pad + local edge index, with pad chosen so that P equals the
@@ -78,11 +73,7 @@ __device__ __forceinline__ bool stop_after(const IterCounters* prev) {
 enum : int {
     kEdgePlain = 0,  // every edge of the list belongs to a processed vertex
     kEdgeCheck = 1,  // full list, skip edges of unprocessed vertices
-    kEdgeSuper = 2,  // superstep: + influence / estatus into the bitmap
-    kEdgeFoldStash = 3,  // superstep pass 1 of the stash scheme: fold + hand every
-                         // run's messages, prefix and vertex marks to the
-                         // influence pass (edge_influence_kernel)
-    kEdgeChain = 4,  // superstep in one pass: fold + influence / estatus, the carry
+    kEdgeChain = 2,  // superstep in one pass: fold + influence / estatus, the carry
                      // into a task's continuing vertex from the chain (chain_carry)
 };
 
@@ -116,17 +107,7 @@ struct EdgeArgs {
     uint32_t cold_last;
     typename P::Accum* __restrict__ acc_out;  // [local vertex]
     typename P::Accum* __restrict__ hv;       // [task] continuing head piece
-    typename P::Accum* __restrict__ tv;       // [task] continuing tail piece
-    const typename P::Accum* __restrict__ carry;  // [task] pass 2: carry into the task
-    // superstep stash (kEdgeFoldStash -> edge_influence_kernel): pass 1
-    // saves every run's gathered messages ([padded position]), the lane's
-    // exclusive in-task prefix of its first vertex ([run]) and its vertex
-    // marks ([run]: bits 0-15 a vertex starts at P0+j, bits 16-31 the edge
-    // belongs to a processed vertex); the influence pass streams them.
-    typename P::Message* __restrict__ stash;
-    typename P::Accum* __restrict__ lane_pre;
-    uint32_t* __restrict__ run_meta;
-    uint32_t* __restrict__ task_info;  // [task] kTaskCont | end of the first vertex
+    typename P::Accum* __restrict__ tv;       // [task] continuing tail piece (chain: inclusive)
     // kEdgeChain: per task {state, value} (16-byte slots, accumulators of <= 8
     // bytes) or the state alone (values in hv / tv), and the task ticket
     ulonglong2* __restrict__ cdesc;
@@ -155,7 +136,6 @@ struct VertexArgs {
     const typename P::Accum* __restrict__ acc_out;
     const typename P::Accum* __restrict__ hv;
     const typename P::Accum* __restrict__ tv;
-    typename P::Accum* __restrict__ carry;            // superstep: carry into task t
     IterCounters* __restrict__ ctr;
     IterCounters* __restrict__ ctr_next;              // reset here for the next iteration
     const IterCounters* stop_if;                      // see EdgeArgs::stop_if
@@ -185,17 +165,6 @@ __device__ __forceinline__ void for_run(F&& f) {
 #pragma unroll
         for (int j = 0; j < kRun; ++j) f(j);
     }
-}
-
-// Stash rows go through WarpRows (coalesced 512-byte accesses) when a run's
-// messages form a power-of-two number of 16-byte chunks that fits 8 KB of
-// shared memory per warp; otherwise lanes store / load their runs directly.
-template <class P>
-__host__ __device__ constexpr int stash_row_bytes() {
-    constexpr int b = (int)sizeof(typename P::Message) * kRun;
-    // static shared memory: 32 rows per warp within 32 KB per block
-    return (b % 16 == 0 && ((b / 16) & (b / 16 - 1)) == 0 && b * 32 * kWarpsPerBlock <= 32768) ? b
-                                                                                                : 0;
 }
 
 template <class W>
@@ -249,10 +218,6 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
     }
 }
 
-// task_info word written by the stash pass 1 (low 16 bits: task-relative
-// end of the task's first vertex, clamped to 513)
-constexpr uint32_t kTaskCont = 1u << 16;  // the first vertex began in an earlier task
-
 // Rewrite the flags of a task's processed edges (lane bits `own`, relative
 // to its run) to `kbits`; flags of edges of skipped vertices persist
 // (engine.hpp:204-211). Warp-collective: the lanes' 16-bit fields are
@@ -279,24 +244,6 @@ __device__ __forceinline__ void warp_write_flags(uint32_t* __restrict__ bitmap, 
         uint32_t* wp = bitmap + (w0 + lane);
         if (s >= 0 && s + 32 <= kChunkEdges) *wp = o == 0xffffffffu ? k : ((*wp & ~o) | k);
         else { atomicAnd(wp, ~o); atomicOr(wp, k); }
-    }
-}
-
-// The superstep hand-over of one task's gathered messages to the stash:
-// warp-collective coalesced rows when the run is a power-of-two number of
-// 16-byte chunks, per-lane stores otherwise.
-template <class P, class W, class MA>
-__device__ __forceinline__ void stash_rows(const EdgeArgs<P, W>& a, char* xs, int lane, uint64_t t,
-                                           const MA& m) {
-    constexpr int RB = stash_row_bytes<P>();
-    if constexpr (RB != 0) {
-        uint4 row[RB / 16];
-        memcpy(row, &m[0], RB);
-        WarpRows<RB>::store(xs, lane, row, reinterpret_cast<uint4*>(a.stash + t * kChunkEdges));
-    } else {
-        const uint64_t P0 = (t * kWarp + lane) * kRun;
-#pragma unroll
-        for (int j = 0; j < kRun; ++j) a.stash[P0 + j] = m[j];
     }
 }
 
@@ -390,19 +337,18 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
     return acc;
 }
 
-template <class P, class W, int MODE, bool PASS2, bool HOT = false>
-__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, char* xs,
+template <class P, class W, int MODE, bool HOT = false>
+__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                                           uint64_t t, int lane, uint64_t pol_stream,
                                           uint64_t pol_hot, uint64_t pol_cold, HotTable ht = {}) {
     using Accum = typename P::Accum;
     using Message = typename P::Message;
-    constexpr bool SUPER = MODE == kEdgeSuper;
     constexpr bool CHAIN = MODE == kEdgeChain;
     const uint64_t tstart = t * kChunkEdges;
     const uint64_t r = t * kWarp + lane;
     const uint64_t P0 = r * kRun;
     const uint64_t lo = P0 > a.pad ? P0 : a.pad;
-    uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
+    const uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
     // non-empty vertices touching the task: [i0, i_next], starts staged
     const uint32_t i0 = a.run_i[t * kWarp];
     Message m[kRun];
@@ -413,7 +359,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     // register-resident runs issue them first so their latency overlaps the
     // staging loads (local-memory runs of heavy programs measured better
     // the other way round).
-    constexpr bool kEarly = !PASS2 && fold_unroll<P>() != 1;
+    constexpr bool kEarly = fold_unroll<P>() != 1;
     if constexpr (kEarly) {
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
@@ -421,23 +367,15 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
-    uint32_t cnt = 2;  // pass 2 only needs the first vertex's start and end
-    if constexpr (!PASS2) {
-        const uint64_t rn = (t + 1) * kWarp;
-        const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
-        cnt = i_next - i0 + 2;  // <= kStageStarts
-    }
+    const uint64_t rn = (t + 1) * kWarp;
+    const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
+    const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
     for (uint32_t j = lane; j < cnt; j += kWarp) {
         const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
         st0[j] = (int16_t)(rel < 0 ? -1 : (rel > kChunkEdges ? kChunkEdges + 1 : rel));
     }
     __syncwarp();
     const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
-    if (PASS2 && !cont) return;    // warp-uniform
-    if constexpr (PASS2) {  // pass 2 only re-walks the continuing first vertex's edges
-        const uint64_t vend = tstart + (uint64_t)(st0[1] > 0 ? st0[1] : 0);
-        if (hi > vend) hi = vend;
-    }
     if constexpr (!kEarly) {
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
@@ -461,7 +399,6 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         if (len > 0) pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
     const bool pk_first = pk;  // lane 0: the task's first vertex
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
-    uint32_t bmask = 0;  // positions where a later vertex of the run starts
     Accum x = a.prog.gather_identity(), hvv = x;
     bool head_closed = false;
     auto fold_step = [&](int j, const Message& mj, double wj) {
@@ -471,13 +408,12 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 if (!head_closed) {
                     hvv = x;
                     head_closed = true;
-                } else if (!PASS2) {
+                } else {
                     a.acc_out[a.nz_vid[i0 + k]] = x;  // began and ended inside this run
                 }
                 x = a.prog.gather_identity();
                 ++k;
                 nb = st0[k + 1];
-                if constexpr (MODE == kEdgeFoldStash) bmask |= 1u << j;
                 if constexpr (MODE != kEdgePlain)
                     pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
             }
@@ -490,10 +426,9 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     // Heavy programs fold the run in a rolled loop (one inlined gather);
     // without a second pass over the messages they shift the run through
     // registers (element 0 each step) instead of indexing a local array.
-    constexpr bool kShift = fold_unroll<P>() == 1 && !SUPER && !CHAIN && !PASS2 &&
+    constexpr bool kShift = fold_unroll<P>() == 1 && !CHAIN &&
                             sizeof(Message) <= 16;  // larger runs stay in local memory
     if constexpr (kShift) {
-        if constexpr (MODE == kEdgeFoldStash) stash_rows<P, W>(a, xs, lane, t, m);  // before the shifts
 #pragma unroll 1
         for (int j = 0; j < kRun; ++j) {
             fold_step(j, m[0], wv(0));
@@ -518,7 +453,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     const Accum prevS = shfl_up_any(S, 1);
     const uint32_t prevK = __shfl_up_sync(0xffffffffu, tk, 1);
     const bool joins_prev = len > 0 && lane > 0 && prevK == (uint32_t)hk;
-    if (!PASS2) {
+    {
         if (head_closed) {
             const Accum hval = joins_prev ? a.prog.combine(prevS, hvv) : hvv;
             if (cont && hk == 0) a.hv[t] = hval;
@@ -569,29 +504,16 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             publish_incl(carry_in);
         }
     }
-    if constexpr (SUPER || CHAIN) {
+    if constexpr (CHAIN) {
         // influence of each edge against its exclusive running prefix
-        // (engine.hpp:204-211); a vertex whose fold began in an earlier task
-        // is handled by pass 2 with that task's carry (kEdgeSuper) or after
-        // the chain look-back (kEdgeChain).
-        Accum run = a.prog.gather_identity();
-        bool skip_head = false;
-        if (cont && hk == 0) {
-            if (CHAIN) {
-                run = carry_in;
-            } else if (PASS2) {
-                run = a.carry[t];
-            } else {
-                skip_head = true;
-            }
-        } else if (PASS2) {
-            skip_head = true;  // pass 2 only rewrites the continuing vertex
-        }
+        // (engine.hpp:204-211): the carry into the task, the run's prefix in
+        // the task, then the run's own sequential gathers; identity at each
+        // later vertex start
+        Accum run = (cont && hk == 0) ? carry_in : a.prog.gather_identity();
         if (joins_prev) run = a.prog.combine(run, prevS);
-        uint32_t kbits = 0, own = pmask;
+        uint32_t kbits = 0;
         int nb2 = len > 0 ? st0[hk + 1] : 0;
         int kk = hk;
-        bool in_head = true;
         for_run<P>([&](int j) {
             const int p = (int)(P0 - tstart) + j;
             if (p >= rlo && p < rhi) {
@@ -599,24 +521,14 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     ++kk;
                     nb2 = st0[kk + 1];
                     run = a.prog.gather_identity();
-                    in_head = false;
                 }
-                const bool mine = in_head ? !skip_head : !PASS2;
-                if (!mine) {
-                    own &= ~(1u << j);
-                } else if ((pmask >> j) & 1u) {
+                if ((pmask >> j) & 1u) {
                     const double infl = a.prog.gather(run, m[j], wv(j));
                     if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
                 }
             }
         });
-        warp_write_flags(a.bitmap, a.pad, tstart, own, kbits, lane);
-    }
-    if constexpr (MODE == kEdgeFoldStash) {
-        if (lane == 0) a.task_info[t] = cont ? (kTaskCont | (uint32_t)st0[1]) : 0u;
-        __stcs(a.run_meta + r, len > 0 ? (bmask | (pmask << 16)) : 0u);
-        if (pmask) a.lane_pre[r] = joins_prev ? prevS : a.prog.gather_identity();
-        if constexpr (!kShift) stash_rows<P, W>(a, xs, lane, t, m);
+        warp_write_flags(a.bitmap, a.pad, tstart, pmask, kbits, lane);
     }
     __syncwarp();  // st0 is restaged by the warp's next task
 }
@@ -626,8 +538,6 @@ __global__ void __launch_bounds__(kBlockThreads)
 edge_kernel(const EdgeArgs<P, W> a) {
     if (stop_after(a.stop_if)) return;
     __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
-    constexpr int RB = MODE == kEdgeFoldStash ? stash_row_bytes<P>() : 0;
-    __shared__ __align__(16) char xs_all[kWarpsPerBlock][RB ? 32 * RB : 16];
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
@@ -638,16 +548,15 @@ edge_kernel(const EdgeArgs<P, W> a) {
             if (lane == 0) t = atomicAdd(a.ticket, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= a.ntasks) break;
-            edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], xs_all[threadIdx.x >> 5], t,
-                                         lane, pol_stream, pol_hot, pol_cold);
+            edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
+                                  pol_cold);
         }
         return;
     }
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
-        edge_task<P, W, MODE, false>(a, st_all[threadIdx.x >> 5], xs_all[threadIdx.x >> 5], t,
-                                     lane, pol_stream, pol_hot, pol_cold);
+        edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot, pol_cold);
     }
 }
 
@@ -676,93 +585,18 @@ edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
     const uint64_t warps = (uint64_t)gridDim.x * kHotWarps;
     for (uint64_t t = (uint64_t)blockIdx.x * kHotWarps + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
-        edge_task<P, W, MODE, false, true>(a, st_all[threadIdx.x >> 5], nullptr, t, lane,
-                                           pol_stream, pol_hot, pol_cold, ht);
-}
-
-template <class P, class W>
-__global__ void __launch_bounds__(kBlockThreads)
-edge_pass2_kernel(const EdgeArgs<P, W> a) {
-    __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
-    const int lane = threadIdx.x & 31;
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_hot = policy_evict_last();
-    const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
-    const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
-    for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
-         t += warps)
-        edge_task<P, W, kEdgeSuper, true>(a, st_all[threadIdx.x >> 5], nullptr, t, lane,
-                                          pol_stream, pol_hot, pol_cold);
-}
-
-// Superstep influence pass of the stash scheme (engine.hpp:204-211): every
-// edge of a processed vertex gets estatus(gather(prefix, message)) with the
-// prefix = the accumulator before the edge in CSC order:
-//   run's first vertex, continuing from an earlier task: carry[t] (+) lane_pre[r]
-//   run's first vertex otherwise:                       lane_pre[r]
-//   later vertices of the run:                          identity at their start
-// then the run's own sequential gathers over the stashed messages -- the
-// arithmetic of the single-kernel superstep (combine with the identity is
-// exact), as a pure stream: no sources, no message gathers, no staging.
-template <class P, class W>
-__global__ void __launch_bounds__(kBlockThreads)
-edge_influence_kernel(const EdgeArgs<P, W> a) {
-    using Accum = typename P::Accum;
-    using Message = typename P::Message;
-    constexpr int RB = stash_row_bytes<P>();
-    __shared__ __align__(16) char xs_all[kWarpsPerBlock][RB ? 32 * RB : 16];
-    char* xs = xs_all[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
-    for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
-         t += warps) {
-        const uint64_t r = t * kWarp + lane;
-        const uint32_t meta = a.run_meta[r];
-        const uint32_t own = meta >> 16;
-        if (!__any_sync(0xffffffffu, own != 0)) continue;  // warp-uniform
-        const uint32_t info = a.task_info[t];
-        const uint64_t P0 = r * kRun;
-        Message mm[kRun];
-        if constexpr (RB != 0) {
-            uint4 row[RB / 16];
-            WarpRows<RB>::load(xs, lane, reinterpret_cast<const uint4*>(a.stash + t * kChunkEdges),
-                               row);
-            memcpy(mm, row, RB);
-        } else {
-            if (own) {
-#pragma unroll
-                for (int j = 0; j < kRun; ++j) mm[j] = a.stash[P0 + j];
-            }
-        }
-        uint32_t kbits = 0;
-        if (own) {
-            const bool head = (info & kTaskCont) && P0 < t * kChunkEdges + (info & 0xffffu);
-            Accum run = a.prog.combine(head ? a.carry[t] : a.prog.gather_identity(), a.lane_pre[r]);
-            for_run<P>([&](int j) {
-                if ((meta >> j) & 1u) run = a.prog.gather_identity();
-                if ((own >> j) & 1u) {
-                    double w = 1.0;
-                    if constexpr (!std::is_void_v<W>) w = (double)a.w[P0 + j];
-                    const double infl = a.prog.gather(run, mm[j], w);
-                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
-                }
-            });
-        }
-        warp_write_flags(a.bitmap, a.pad, t * kChunkEdges, own, kbits, lane);
-    }
+        edge_task<P, W, MODE, true>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
+                                    pol_cold, ht);
 }
 
 // Vertex epilogue: the accumulator of vertex v is acc_out[v] when its list
 // lies inside one task, else tv[t0] (+) hv[t0+1] (+) ... (+) hv[t1] in task
 // order; then GG-Apply, GG-VStatus, valid, message, status, counters.
-// VK: kVtxPlain, kVtxCarry (superstep, stash / pass-2 schemes: also writes
-// carry[t]), kVtxChain (superstep, chain scheme: tv[t1-1] already holds the
-// left-to-right fold up to task t1-1, so the join is one combine).
-enum : int { kVtxPlain = 0, kVtxCarry = 1, kVtxChain = 2 };
-template <class P, class W, int VK>
+// SUPER: after a kEdgeChain superstep tv[t1-1] already holds the
+// left-to-right fold up to task t1-1, so the join is one combine.
+template <class P, class W, bool SUPER>
 __global__ void __launch_bounds__(256)
 vertex_kernel(const VertexArgs<P, W> a) {
-    constexpr bool SUPER = VK != kVtxPlain;
     using Accum = typename P::Accum;
     using Property = typename P::Property;
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // the next iteration's counters, even if skipped
@@ -814,14 +648,11 @@ vertex_kernel(const VertexArgs<P, W> a) {
                                    t1 = (o1[i] - 1 + a.pad) / kChunkEdges;
                     if (t0 == t1) {
                         acc = acc1[i];
-                    } else if constexpr (VK == kVtxChain) {
+                    } else if constexpr (SUPER) {
                         acc = a.prog.combine(a.tv[t1 - 1], a.hv[t1]);
                     } else {
                         acc = a.tv[t0];
-                        for (uint64_t t = t0 + 1; t <= t1; ++t) {
-                            if constexpr (VK == kVtxCarry) a.carry[t] = acc;
-                            acc = a.prog.combine(acc, a.hv[t]);
-                        }
+                        for (uint64_t t = t0 + 1; t <= t1; ++t) acc = a.prog.combine(acc, a.hv[t]);
                     }
                 }
                 const Property fresh = a.prog.apply(v, acc, prev[i], a.n);  // GG-Apply (:216)
