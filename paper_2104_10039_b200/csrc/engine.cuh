@@ -160,6 +160,18 @@ struct Engine {
         GGB_CUDA(cudaGetLastError());
     }
 
+    static void launch_chain(DevGraph& g, const EdgeArgs<P, W>& ea) {
+        if constexpr (chain_bounded<P, W>()) {
+            static int grid = 0;
+            if (!grid) grid = occupancy_grid((const void*)edge_chain_kernel<P, W>, kBlockThreads, 0,
+                                             g.num_sms);
+            edge_chain_kernel<P, W><<<grid, kBlockThreads, 0, g.stream>>>(ea);
+            GGB_CUDA(cudaGetLastError());
+        } else {
+            launch_edge<kEdgeChain>(g, ea);
+        }
+    }
+
     static void run(DevGraph& g, const P& prog, RunIO& io) {
         const gg_engine_config& cfg = *io.cfg;
         const bool timing = io.opts && io.opts->timing;
@@ -322,7 +334,7 @@ struct Engine {
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
                 if (super) {
                     GGB_CUDA(cudaMemsetAsync(chain, 0, L.ntasks * kSlot + 4, g.stream));
-                    launch_edge<kEdgeChain>(g, ea);
+                    launch_chain(g, ea);
                 } else if (all_proc && nhot) {
                     if constexpr (kHotOK) launch_edge_hot(g, ea, nhot);
                 }
