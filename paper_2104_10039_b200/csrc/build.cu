@@ -12,6 +12,7 @@
 
 #include "exchange.cuh"
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "graph.cuh"
@@ -68,36 +69,45 @@ __device__ __forceinline__ bool keep_edge(uint64_t x, uint64_t T) {
     return (xf ^ (xf >> 31)) < T;
 }
 
+// Flags of bitmap word i (engine.cpp:63-75); e_base = global id of local edge 0.
+__device__ __forceinline__ uint32_t sparsify_word(uint64_t i, uint64_t e_loc, uint64_t e_base,
+                                                  uint64_t T, uint64_t key, int keep_all) {
+    const uint64_t e0 = i * 32;
+    const int nb = e_loc - e0 < 32 ? (int)(e_loc - e0) : 32;
+    uint32_t word = 0;
+    if (keep_all) {
+        word = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    } else if (nb == 32 && (e_base & 31) == 0) {  // key ^ (base | b) = (key ^ base) ^ b
+        const uint64_t k0 = key ^ (e_base + e0);
+#pragma unroll 8
+        for (int b = 0; b < 32; ++b) word |= (keep_edge(k0 ^ (uint64_t)b, T) ? 1u : 0u) << b;
+    } else {
+        for (int b = 0; b < nb; ++b) word |= (keep_edge(key ^ (e_base + e0 + b), T) ? 1u : 0u) << b;
+    }
+    return word;
+}
+
 __global__ void sparsify_kernel(uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_loc,
                                 uint64_t e_base, uint64_t T, uint64_t key, int keep_all) {
-    const bool aligned = (e_base & 31) == 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nwords;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t word = 0;
-        if (i < nwords) {
-            const uint64_t e0 = i * 32;
-            const int nb = e_loc - e0 < 32 ? (int)(e_loc - e0) : 32;
-            if (keep_all) {
-                word = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
-            } else if (nb == 32 && aligned) {  // key ^ (base | b) = (key ^ base) ^ b
-                const uint64_t k0 = key ^ (e_base + e0);
-#pragma unroll 8
-                for (int b = 0; b < 32; ++b) word |= (keep_edge(k0 ^ (uint64_t)b, T) ? 1u : 0u) << b;
-            } else {
-                for (int b = 0; b < nb; ++b)
-                    word |= (keep_edge(key ^ (e_base + e0 + b), T) ? 1u : 0u) << b;
-            }
-        }
-        bitmap[i] = word;  // bitmap[nwords] is the zero guard word
-    }
+         i += (uint64_t)gridDim.x * blockDim.x)
+        bitmap[i] = i < nwords ? sparsify_word(i, e_loc, e_base, T, key, keep_all) : 0u;  // [nwords]: zero guard word
+}
+
+SparsifySpec sparsify_spec(double sigma, uint64_t seed, bool all_ones) {
+    const uint64_t thr = all_ones ? (1ull << 53) : (uint64_t)std::ceil(sigma * 0x1.0p53);
+    SparsifySpec h;
+    h.keep_all = thr >= (1ull << 53) ? 1 : 0;  // (h >> 11) < 2^53 always
+    h.T = h.keep_all ? 0 : thr << 11;
+    h.key = mix64(seed);
+    return h;
 }
 
 void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
-    const uint64_t thr = all_ones ? (1ull << 53) : (uint64_t)std::ceil(sigma * 0x1.0p53);
-    const int keep_all = thr >= (1ull << 53) ? 1 : 0;  // (h >> 11) < 2^53 always
+    const SparsifySpec h = sparsify_spec(sigma, seed, all_ones);
     sparsify_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(
-        bitmap, nwords, g.e_loc, g.e_base, keep_all ? 0 : thr << 11, mix64(seed), keep_all);
+        bitmap, nwords, g.e_loc, g.e_base, h.T, h.key, h.keep_all);
     GGB_CUDA(cudaGetLastError());
 }
 
@@ -238,18 +248,212 @@ __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __r
     }
 }
 
+// Single-pass flags -> prefix -> compaction (one rank). A CTA takes a tile of
+// kScanTile bitmap words (tiles claimed in order from a ticket; warp w owns
+// the tile's words [128w, 128w + 128), lane l words 32j + l), computes the
+// words (HASH: the sparsify hash; otherwise read from the bitmap), scans their
+// popcounts, gets the tile's exclusive prefix by a decoupled look-back over
+// the earlier tiles' {flag, value} words (one 64-bit relaxed store each: no
+// fence), writes the per-word prefix `wpref` (for soff_kernel) and compacts
+// the tile's kept sources / weights. Replaces sparsify + popc + scan +
+// compact (four passes; the sources are read once).
+constexpr int kScanThreads = 256, kScanWPL = 4;             // words per lane
+constexpr int kScanTile = kScanThreads * kScanWPL;          // words per tile
+constexpr int kScanWarpWords = 32 * kScanWPL;
+constexpr uint64_t kScanAgg = 1ull << 62, kScanIncl = 2ull << 62, kScanVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Held to 6 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8): the hash
+// variant is issue-bound and needs the warps (c5: 5.66 -> 4.69 ms).
+template <int WB, bool HASH>
+__global__ void __launch_bounds__(kScanThreads, WB == 0 ? 6 : WB == 4 ? 4 : 3)
+scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w, uint64_t e_loc,
+                    uint64_t in_pad, uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_base,
+                    SparsifySpec h, uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
+                    void* __restrict__ s_w, unsigned long long* __restrict__ tstate,
+                    uint32_t* __restrict__ ticket, uint64_t ntiles) {
+    using WT = std::conditional_t<WB == 8, unsigned long long, uint32_t>;
+    constexpr int kWarps = kScanThreads / 32;
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_wsum[kWarps];
+    __shared__ uint64_t s_wbase[kWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= ntiles) break;
+        const uint64_t w0 = t * kScanTile + (uint64_t)warp * kScanWarpWords;
+        // sources of 8 words (lane l: edge l of each), loaded one batch ahead;
+        // the first batch before the flags and the look-back
+        uint32_t sv[2][8];
+        WT wv[2][8];
+        auto load_batch = [&](int k0, uint32_t (&s8)[8], WT (&w8)[8]) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t e = (w0 + k0 + k) * 32 + lane;
+                const bool ine = e < e_loc;
+                s8[k] = ine ? __ldg(src + in_pad + e) : 0u;
+                if constexpr (WB != 0) w8[k] = ine ? __ldg(static_cast<const WT*>(w) + in_pad + e) : WT(0);
+            }
+        };
+        load_batch(0, sv[0], wv[0]);
+        uint32_t word[kScanWPL], off[kScanWPL];  // off: exclusive popcount within the warp
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < kScanWPL; ++j) {
+            const uint64_t wi = w0 + 32 * j + lane;
+            uint32_t x = 0;
+            if constexpr (HASH) {
+                if (wi < nwords) x = sparsify_word(wi, e_loc, e_base, h.T, h.key, h.keep_all);
+                if (wi <= nwords) bitmap[wi] = x;  // [nwords]: zero guard word
+            } else {
+                if (wi < nwords) x = __ldg(bitmap + wi);
+            }
+            word[j] = x;
+            uint32_t incl = __popc(x);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            off[j] = run + incl - __popc(x);
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_wsum[warp] = run;
+        __syncthreads();
+        if (warp == 0) {
+            const uint64_t ws = lane < kWarps ? s_wsum[lane] : 0u;
+            uint64_t wincl = ws;
+#pragma unroll
+            for (int o = 1; o < kWarps; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, wincl, o);
+                if (lane >= o) wincl += y;
+            }
+            const uint64_t agg = __shfl_sync(0xffffffffu, wincl, kWarps - 1);
+            if (lane == 0) st_relaxed_u64(tstate + t, (t == 0 ? kScanIncl : kScanAgg) | agg);
+            // look-back: lane i reads tile j - i; the nearest inclusive value
+            // ends the walk (tiles before 0 count as inclusive 0)
+            uint64_t excl = 0;
+            for (int64_t j = (int64_t)t - 1; j >= 0; j -= 32) {
+                const int64_t q = j - lane;
+                uint64_t st;
+                do {
+                    st = q >= 0 ? ld_relaxed_u64(tstate + q) : kScanIncl;
+                } while (__any_sync(0xffffffffu, (st >> 62) == 0));
+                const uint32_t im = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+                uint64_t v = st & kScanVal;
+                if (im) v = lane <= __ffs(im) - 1 ? v : 0ull;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (im) break;
+            }
+            if (t && lane == 0) st_relaxed_u64(tstate + t, kScanIncl | (excl + agg));
+            if (lane < kWarps) s_wbase[lane] = excl + wincl - ws;  // warp's exclusive base
+        }
+        __syncthreads();
+        const uint64_t wbase = s_wbase[warp];
+#pragma unroll
+        for (int j = 0; j < kScanWPL; ++j) {
+            const uint64_t wi = w0 + 32 * j + lane;
+            if (wi <= nwords) wpref[wi] = wbase + off[j];  // wpref[nwords] = kept total
+        }
+#pragma unroll
+        for (int b = 0; b < kScanWarpWords / 8; ++b) {
+            if (w0 + 8 * b >= nwords) break;
+            if (b + 1 < kScanWarpWords / 8) load_batch(8 * (b + 1), sv[(b + 1) & 1], wv[(b + 1) & 1]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int kw = 8 * b + k;  // word of the warp: lane kw % 32 of word[kw / 32]
+                const uint32_t wk = __shfl_sync(0xffffffffu, word[kw / 32], kw % 32);
+                const uint32_t ok = __shfl_sync(0xffffffffu, off[kw / 32], kw % 32);
+                if ((wk >> lane) & 1u) {
+                    const uint64_t pos = wbase + ok + (uint32_t)__popc(wk & lt);
+                    s_src[pos] = sv[b & 1][k];
+                    if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[b & 1][k];
+                }
+            }
+        }
+        __syncthreads();  // s_tile / s_wsum / s_wbase reuse
+    }
+}
+
+template <bool HASH>
+static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpec& h,
+                                uint64_t* wpref, uint32_t* s_src, void* s_w) {
+    const uint64_t nwords = (g.e_loc + 31) / 32;
+    const uint64_t ntiles = (nwords + 1 + kScanTile - 1) / kScanTile;
+    auto* tstate = g.ws.get<unsigned long long>("rb.tstate", ntiles + 1);
+    auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
+    GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
+    const size_t wb = weight_size(g.wkind);
+    const void* k = wb == 0 ? (const void*)scan_compact_kernel<0, HASH>
+                  : wb == 4 ? (const void*)scan_compact_kernel<4, HASH>
+                            : (const void*)scan_compact_kernel<8, HASH>;
+    static int per_sm[2][3] = {};
+    int& ps = per_sm[HASH][wb == 0 ? 0 : wb == 4 ? 1 : 2];
+    if (!ps) ps = occupancy_grid(k, kScanThreads, 0, 1);
+    const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)ps * g.num_sms);
+    if (wb == 0)
+        scan_compact_kernel<0, HASH><<<gr, kScanThreads, 0, g.stream>>>(
+            g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
+            ticket, ntiles);
+    else if (wb == 4)
+        scan_compact_kernel<4, HASH><<<gr, kScanThreads, 0, g.stream>>>(
+            g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
+            ticket, ntiles);
+    else
+        scan_compact_kernel<8, HASH><<<gr, kScanThreads, 0, g.stream>>>(
+            g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
+            ticket, ntiles);
+    GGB_CUDA(cudaGetLastError());
+}
+
 uint64_t sparse_pad(DevGraph& g, uint64_t kept_local) {
     if (g.nranks <= 1) return 0;
     return exchange_exclusive_base(g, kept_local) % kChunkEdges;
 }
 
-uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
+uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
                         void* s_w, ListMeta& meta, cudaEvent_t ev0, cudaEvent_t ev1,
-                        int* launches) {
+                        int* launches, const SparsifySpec* hash) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
-    uint64_t* cnt = g.ws.get<uint64_t>("rb.cnt", nwords + 1);
     uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
     if (ev0) GGB_CUDA(cudaEventRecord(ev0, g.stream));
+    uint64_t kept = 0;
+    if (g.nranks == 1) {
+        // one pass: (sparsify +) scan + compaction at pad 0
+        if (hash) launch_scan_compact<true>(g, bitmap, *hash, wpref, s_src, s_w);
+        else launch_scan_compact<false>(g, bitmap, SparsifySpec{}, wpref, s_src, s_w);
+        soff_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref,
+                                                                      s_off);
+        GGB_CUDA(cudaGetLastError());
+        GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        build_runs(g, s_off, 0, kept, "sp", meta);
+        if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
+        if (launches) *launches += 6;
+        return kept;
+    }
+    // several ranks: the list's padded base needs the kept counts of all
+    // ranks before compaction
+    if (hash) {
+        sparsify_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(
+            bitmap, nwords, g.e_loc, g.e_base, hash->T, hash->key, hash->keep_all);
+        GGB_CUDA(cudaGetLastError());
+        if (launches) ++*launches;
+    }
+    uint64_t* cnt = g.ws.get<uint64_t>("rb.cnt", nwords + 1);
     popc_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(bitmap, nwords, cnt);
     GGB_CUDA(cudaGetLastError());
     size_t tmp = 0;
@@ -259,7 +463,6 @@ uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, ui
     soff_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref,
                                                                   s_off);
     GGB_CUDA(cudaGetLastError());
-    uint64_t kept = 0;
     GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     const uint64_t pad = sparse_pad(g, kept);
@@ -288,12 +491,19 @@ uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, ui
 // --------------------------------------------------------------------------
 __global__ void slot_key_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
                                 const uint64_t* __restrict__ bounds, int nranks,
-                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int qbits) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t r = 0;
         while (r + 1 < (uint64_t)nranks && v >= bounds[r + 1]) ++r;
-        keys[v] = (r << 32) | (uint64_t)(0xffffffffu - outdeg[v]);  // rank, then out-degree desc
+        const uint32_t d = outdeg[v];
+        uint32_t h = d;
+        if (qbits >= 0 && d) {  // degree class: floor(log2 d) and the next qbits bits
+            const int lz = 31 - __clz(d);
+            const uint32_t frac = qbits ? ((d << (31 - lz)) >> (31 - qbits)) & ((1u << qbits) - 1u) : 0u;
+            h = 1u + ((uint32_t)lz << qbits) + frac;
+        }
+        keys[v] = (r << 32) | (uint64_t)(0xffffffffu - h);  // rank, then out-degree (class) desc
         vals[v] = (uint32_t)v;
     }
 }
@@ -341,7 +551,9 @@ void compute_slots(DevGraph& g) {
     db = static_cast<decltype(db)>(dev_alloc(g.bounds.size() * 8, g.stream));
     GGB_CUDA(cudaMemcpyAsync(db, g.bounds.data(), g.bounds.size() * 8, cudaMemcpyHostToDevice,
                              g.stream));
-    slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, k0, v0);
+    int qbits = 0;  // octave classes (GGB_SLOT_QBITS: -1 exact degree, q > 0 finer classes)
+    if (const char* e = std::getenv("GGB_SLOT_QBITS")) qbits = std::atoi(e);
+    slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, k0, v0, qbits);
     GGB_CUDA(cudaGetLastError());
     int rank_bits = 0;
     while ((1 << rank_bits) < g.nranks) ++rank_bits;

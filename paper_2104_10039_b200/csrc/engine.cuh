@@ -224,9 +224,8 @@ struct Engine {
             s_off = ws.get<uint64_t>("s_off", nloc + 1);
             s_src = ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
             s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
-            sparsify_bitmap(g, bitmap, cfg.sigma, cfg.seed, false);
-            ++launches;
-            kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches);
+            const SparsifySpec hs = sparsify_spec(cfg.sigma, cfg.seed, false);
+            kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches, &hs);
         }
         const uint64_t* a_off = sparse ? s_off : g.off;
         // the hottest message slots (lowest ids: hot-first layout) are pinned in

@@ -165,11 +165,18 @@ void export_sources(const DevGraph& g, uint32_t* host_out);
 // Size `meta` for (pad, e) and build its run -> vertex map from `off`.
 void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e,
                 const std::string& tag, ListMeta& meta);
+// engine.cpp:63-75 as the integer test mix64(key ^ e) < T (keep_all: sigma >= 1)
+struct SparsifySpec {
+    uint64_t T = 0, key = 0;
+    int keep_all = 0;
+};
+SparsifySpec sparsify_spec(double sigma, uint64_t seed, bool all_ones);
 // flags -> sparsified CSC (s_off, padded s_src/s_w) + its run map. Returns
-// the kept (local) edge count.
-uint64_t rebuild_sparse(DevGraph& g, const uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
+// the kept (local) edge count. With `hash`, the flags are first computed
+// into `bitmap` (the initial sparsify, engine.hpp:154-161).
+uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
                         void* s_w, ListMeta& meta, cudaEvent_t ev0, cudaEvent_t ev1,
-                        int* launches);
+                        int* launches, const SparsifySpec* hash = nullptr);
 // padded-position base of the sparsified list of this rank (exclusive scan
 // of kept counts over ranks, modulo the task size); 0 on one GPU.
 uint64_t sparse_pad(DevGraph& g, uint64_t kept_local);

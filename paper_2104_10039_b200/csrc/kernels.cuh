@@ -523,8 +523,12 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     run = a.prog.gather_identity();
                 }
                 if ((pmask >> j) & 1u) {
-                    const double infl = a.prog.gather(run, m[j], wv(j));
-                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
+                    bool keep;
+                    if constexpr (requires { a.prog.gather_keep(run, m[j], wv(j), a.theta); })
+                        keep = a.prog.gather_keep(run, m[j], wv(j), a.theta);
+                    else
+                        keep = a.prog.estatus(a.prog.gather(run, m[j], wv(j)), a.theta);
+                    if (keep) kbits |= 1u << j;
                 }
             }
         });
