@@ -338,7 +338,7 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
 }
 
 template <class P, class W, int MODE, bool HOT = false>
-__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
+__device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint8_t* sp0,
                                           uint64_t t, int lane, uint64_t pol_stream,
                                           uint64_t pol_hot, uint64_t pol_cold, HotTable ht = {}) {
     using Accum = typename P::Accum;
@@ -373,6 +373,10 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     for (uint32_t j = lane; j < cnt; j += kWarp) {
         const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
         st0[j] = (int16_t)(rel < 0 ? -1 : (rel > kChunkEdges ? kChunkEdges + 1 : rel));
+        // skip test of the task's vertices (engine.hpp:196), staged with the
+        // starts so the fold does not wait on it at every vertex boundary
+        if constexpr (MODE != kEdgePlain)
+            if (j + 1 < cnt) sp0[j] = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + j]) ? 1 : 0;
     }
     __syncwarp();
     const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
@@ -396,7 +400,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     int nb = len > 0 ? st0[k + 1] : 0;
     bool pk = true;
     if constexpr (MODE != kEdgePlain)
-        if (len > 0) pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
+        if (len > 0) pk = sp0[k];
     const bool pk_first = pk;  // lane 0: the task's first vertex
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
     Accum x = a.prog.gather_identity(), hvv = x;
@@ -414,8 +418,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 x = a.prog.gather_identity();
                 ++k;
                 nb = st0[k + 1];
-                if constexpr (MODE != kEdgePlain)
-                    pk = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + k]);
+                if constexpr (MODE != kEdgePlain) pk = sp0[k];
             }
             if (pk) {
                 (void)a.prog.gather(x, mj, wj);
@@ -523,12 +526,8 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     run = a.prog.gather_identity();
                 }
                 if ((pmask >> j) & 1u) {
-                    bool keep;
-                    if constexpr (requires { a.prog.gather_keep(run, m[j], wv(j), a.theta); })
-                        keep = a.prog.gather_keep(run, m[j], wv(j), a.theta);
-                    else
-                        keep = a.prog.estatus(a.prog.gather(run, m[j], wv(j)), a.theta);
-                    if (keep) kbits |= 1u << j;
+                    const double infl = a.prog.gather(run, m[j], wv(j));
+                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
                 }
             }
         });
@@ -542,6 +541,8 @@ __global__ void __launch_bounds__(kBlockThreads)
 edge_kernel(const EdgeArgs<P, W> a) {
     if (stop_after(a.stop_if)) return;
     __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
+    __shared__ uint8_t sp_all[MODE == kEdgePlain ? 1 : kWarpsPerBlock][kStageStarts];
+    uint8_t* sp0 = MODE == kEdgePlain ? nullptr : sp_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
@@ -552,7 +553,7 @@ edge_kernel(const EdgeArgs<P, W> a) {
             if (lane == 0) t = atomicAdd(a.ticket, 1u);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= a.ntasks) break;
-            edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
+            edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], sp0, t, lane, pol_stream, pol_hot,
                                   pol_cold);
         }
         return;
@@ -560,7 +561,8 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t warps = (uint64_t)gridDim.x * kWarpsPerBlock;
     for (uint64_t t = (uint64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5); t < a.ntasks;
          t += warps) {
-        edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot, pol_cold);
+        edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], sp0, t, lane, pol_stream, pol_hot,
+                              pol_cold);
     }
 }
 
@@ -578,6 +580,7 @@ template <class P, class W>
 __global__ void __launch_bounds__(kBlockThreads, 6)
 edge_chain_kernel(const EdgeArgs<P, W> a) {
     __shared__ int16_t st_all[kWarpsPerBlock][kStageStarts];
+    __shared__ uint8_t sp_all[kWarpsPerBlock][kStageStarts];
     const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
@@ -587,7 +590,8 @@ edge_chain_kernel(const EdgeArgs<P, W> a) {
         if (lane == 0) t = atomicAdd(a.ticket, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= a.ntasks) break;
-        edge_task<P, W, kEdgeChain>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
+        edge_task<P, W, kEdgeChain>(a, st_all[threadIdx.x >> 5], sp_all[threadIdx.x >> 5], t, lane,
+                                    pol_stream, pol_hot,
                                     pol_cold);
     }
 }
@@ -600,6 +604,7 @@ constexpr int kHotWarps = 24;
 template <class P, class W, int MODE>
 __global__ void __launch_bounds__(kHotWarps * 32, 1)
 edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
+    static_assert(MODE == kEdgePlain, "the hot-table gather has no skip test");
     if (stop_after(a.stop_if)) return;
     using Message = typename P::Message;
     extern __shared__ __align__(16) unsigned char hot_raw[];
@@ -617,7 +622,7 @@ edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
     const uint64_t warps = (uint64_t)gridDim.x * kHotWarps;
     for (uint64_t t = (uint64_t)blockIdx.x * kHotWarps + (threadIdx.x >> 5); t < a.ntasks;
          t += warps)
-        edge_task<P, W, MODE, true>(a, st_all[threadIdx.x >> 5], t, lane, pol_stream, pol_hot,
+        edge_task<P, W, MODE, true>(a, st_all[threadIdx.x >> 5], nullptr, t, lane, pol_stream, pol_hot,
                                     pol_cold, ht);
 }
 

@@ -41,24 +41,6 @@ struct PageRank {
         acc = acc + m;
         return acc > 0.0 ? (acc - before) / acc : 0.0;
     }
-    // estatus(gather(acc, m, w), theta) with the same acc update, deciding
-    // (acc - before) / acc > theta without the division unless the quotient
-    // lies within 2^-48 (relative) of theta: with p = fl(theta * acc) normal
-    // and theta > 0, d > fl(p (1 + 2^-48)) implies d / acc > theta (1 + 2^-49),
-    // so the correctly rounded quotient exceeds theta; symmetrically below.
-    // Bit-identical decisions to the reference's division (superstep flags).
-    __device__ bool gather_keep(Accum& acc, const Message& m, double, double theta) const {
-        const double before = acc;
-        acc = acc + m;
-        if (!(acc > 0.0)) return 0.0 > theta;
-        const double d = acc - before;
-        const double p = theta * acc;
-        if (p >= 0x1p-1000 && p <= 0x1p1000) {
-            if (d > p * (1.0 + 0x1p-48)) return true;
-            if (d < p * (1.0 - 0x1p-48)) return false;
-        }
-        return d / acc > theta;
-    }
     __device__ Accum combine(const Accum& a, const Accum& b) const { return a + b; }
     __device__ Property apply(uint32_t, const Accum& acc, const Property&, uint64_t n) const {
         return (1.0 - damping) / (double)n + damping * acc;  // :31-34
