@@ -132,6 +132,7 @@ __global__ void nonempty_fill_kernel(const uint64_t* __restrict__ off, uint64_t 
          v += (uint64_t)gridDim.x * blockDim.x) {
         if (v == nloc) {
             nz_start[idx[nloc]] = off[nloc];  // sentinel: end of the last vertex
+            marks[nruns] = idx[nloc] ? idx[nloc] - 1 : 0u;  // copied to run_i[nruns] below
             continue;
         }
         if (off[v + 1] <= off[v]) continue;
@@ -180,6 +181,8 @@ void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e, cons
     if (!meta.nruns) return;
     GGB_CUDA(cub::DeviceScan::InclusiveScan(tmpp, tmp2, marks, meta.run_i, MaxU32{}, meta.nruns,
                                             g.stream));
+    GGB_CUDA(cudaMemcpyAsync(meta.run_i + meta.nruns, marks + meta.nruns, 4, cudaMemcpyDeviceToDevice,
+                             g.stream));  // sentinel run_i[nruns] = nz - 1
 }
 
 // --------------------------------------------------------------------------
@@ -197,14 +200,6 @@ __device__ __forceinline__ uint64_t bit_rank(const uint32_t* bitmap, const uint6
     const uint64_t w = e >> 5;
     const uint32_t b = (uint32_t)(e & 31);
     return wpref[w] + (uint64_t)__popc(bitmap[w] & ((1u << b) - 1u));
-}
-
-__global__ void soff_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
-                            const uint32_t* __restrict__ bitmap,
-                            const uint64_t* __restrict__ wpref, uint64_t* __restrict__ s_off) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= nloc;
-         v += (uint64_t)gridDim.x * blockDim.x)
-        s_off[v] = bit_rank(bitmap, wpref, off[v]);
 }
 
 // Stream compaction of the kept edges (sources, weights) into the padded
@@ -254,7 +249,7 @@ __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __r
 // words (HASH: the sparsify hash; otherwise read from the bitmap), scans their
 // popcounts, gets the tile's exclusive prefix by a decoupled look-back over
 // the earlier tiles' {flag, value} words (one 64-bit relaxed store each: no
-// fence), writes the per-word prefix `wpref` (for soff_kernel) and compacts
+// fence), writes the per-word prefix `wpref` (for the list layout) and compacts
 // the tile's kept sources / weights. Replaces sparsify + popc + scan +
 // compact (four passes; the sources are read once).
 constexpr int kScanThreads = 256, kScanWPL = 4;             // words per lane
@@ -269,6 +264,32 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const unsigned long long* p) 
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Decoupled look-back of tile t (one warp): publishes the tile's aggregate,
+// walks back over earlier tiles (lane i reads tile j - i; the nearest
+// inclusive value ends the walk, tiles before 0 count as inclusive 0),
+// publishes the inclusive prefix and returns the exclusive one.
+__device__ __forceinline__ uint64_t tile_lookback(unsigned long long* tstate, uint64_t t,
+                                                  uint64_t agg, int lane) {
+    if (lane == 0) st_relaxed_u64(tstate + t, (t == 0 ? kScanIncl : kScanAgg) | agg);
+    uint64_t excl = 0;
+    for (int64_t j = (int64_t)t - 1; j >= 0; j -= 32) {
+        const int64_t q = j - lane;
+        uint64_t st;
+        do {
+            st = q >= 0 ? ld_relaxed_u64(tstate + q) : kScanIncl;
+        } while (__any_sync(0xffffffffu, (st >> 62) == 0));
+        const uint32_t im = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        uint64_t v = st & kScanVal;
+        if (im) v = lane <= __ffs(im) - 1 ? v : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (im) break;
+    }
+    if (t && lane == 0) st_relaxed_u64(tstate + t, kScanIncl | (excl + agg));
+    return excl;
 }
 
 // Held to 6 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8): the hash
@@ -340,25 +361,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 if (lane >= o) wincl += y;
             }
             const uint64_t agg = __shfl_sync(0xffffffffu, wincl, kWarps - 1);
-            if (lane == 0) st_relaxed_u64(tstate + t, (t == 0 ? kScanIncl : kScanAgg) | agg);
-            // look-back: lane i reads tile j - i; the nearest inclusive value
-            // ends the walk (tiles before 0 count as inclusive 0)
-            uint64_t excl = 0;
-            for (int64_t j = (int64_t)t - 1; j >= 0; j -= 32) {
-                const int64_t q = j - lane;
-                uint64_t st;
-                do {
-                    st = q >= 0 ? ld_relaxed_u64(tstate + q) : kScanIncl;
-                } while (__any_sync(0xffffffffu, (st >> 62) == 0));
-                const uint32_t im = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-                uint64_t v = st & kScanVal;
-                if (im) v = lane <= __ffs(im) - 1 ? v : 0ull;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                excl += v;
-                if (im) break;
-            }
-            if (t && lane == 0) st_relaxed_u64(tstate + t, kScanIncl | (excl + agg));
+            const uint64_t excl = tile_lookback(tstate, t, agg, lane);
             if (lane < kWarps) s_wbase[lane] = excl + wincl - ws;  // warp's exclusive base
         }
         __syncthreads();
@@ -419,6 +422,127 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     GGB_CUDA(cudaGetLastError());
 }
 
+// Sparsified-list layout in one pass over the owned vertices (replaces
+// soff + nonempty flag / scan / fill of build_runs): s_off[v] = rank of
+// off[v] among the kept edges; the non-empty vertices get consecutive nz
+// indices (decoupled look-back over tiles of kLayoutTile vertices; warp w
+// owns the tile's vertices [128w, 128w + 128), lane l vertices 32j + l) with
+// nz_vid / nz_start and the run marks of nonempty_fill_kernel; the thread
+// holding v = nloc writes the sentinels nz_start[nz] and run_i[nruns] = nz - 1.
+constexpr int kLayoutVPT = 4;  // vertices per thread
+constexpr int kLayoutTile = 256 * kLayoutVPT;
+
+__global__ void __launch_bounds__(256)
+sp_layout_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
+                 const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ wpref,
+                 uint64_t pad, uint64_t nruns, uint64_t* __restrict__ s_off,
+                 uint32_t* __restrict__ nz_vid, uint64_t* __restrict__ nz_start,
+                 uint32_t* __restrict__ marks, uint32_t* __restrict__ run_i,
+                 unsigned long long* __restrict__ tstate, uint32_t* __restrict__ ticket,
+                 uint64_t ntiles) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_wsum[8];
+    __shared__ uint64_t s_wbase[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s_tile;
+        if (t >= ntiles) break;
+        const uint64_t vb = t * kLayoutTile + (uint64_t)warp * 32 * kLayoutVPT;  // warp's first vertex
+        uint64_t so[kLayoutVPT];
+#pragma unroll
+        for (int j = 0; j < kLayoutVPT; ++j) {
+            const uint64_t v = vb + 32 * j + lane;
+            so[j] = v <= nloc ? bit_rank(bitmap, wpref, __ldg(off + v)) : 0ull;
+        }
+        const uint64_t vend = vb + 32 * kLayoutVPT;  // lane 31's last successor
+        const uint64_t so_end = (lane == 31 && vend <= nloc) ? bit_rank(bitmap, wpref, __ldg(off + vend)) : 0ull;
+        uint32_t fl = 0, off_in[kLayoutVPT], run = 0;
+#pragma unroll
+        for (int j = 0; j < kLayoutVPT; ++j) {
+            const uint64_t v = vb + 32 * j + lane;
+            uint64_t nx = __shfl_down_sync(0xffffffffu, so[j], 1);
+            const uint64_t nx0 = __shfl_sync(0xffffffffu, j + 1 < kLayoutVPT ? so[j + 1 < kLayoutVPT ? j + 1 : j] : so_end, 0);
+            if (lane == 31) nx = j + 1 < kLayoutVPT ? nx0 : so_end;
+            const bool f = v < nloc && nx > so[j];
+            fl |= (f ? 1u : 0u) << j;
+            const uint32_t b = __ballot_sync(0xffffffffu, f);
+            off_in[j] = run + __popc(b & ((1u << lane) - 1u));
+            run += __popc(b);
+        }
+        if (lane == 0) s_wsum[warp] = run;
+        __syncthreads();
+        if (warp == 0) {
+            const uint64_t ws = lane < 8 ? s_wsum[lane] : 0u;
+            uint64_t wincl = ws;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, wincl, o);
+                if (lane >= o) wincl += y;
+            }
+            const uint64_t agg = __shfl_sync(0xffffffffu, wincl, 7);
+            const uint64_t excl = tile_lookback(tstate, t, agg, lane);
+            if (lane < 8) s_wbase[lane] = excl + wincl - ws;
+        }
+        __syncthreads();
+        const uint64_t wbase = s_wbase[warp];
+#pragma unroll
+        for (int j = 0; j < kLayoutVPT; ++j) {
+            const uint64_t v = vb + 32 * j + lane;
+            if (v > nloc) break;
+            s_off[v] = so[j];
+            const uint64_t i = wbase + off_in[j];
+            if (v == nloc) {  // sentinels: i = nz
+                nz_start[i] = so[j];
+                run_i[nruns] = i ? (uint32_t)(i - 1) : 0u;
+            } else if ((fl >> j) & 1u) {
+                nz_vid[i] = (uint32_t)v;
+                nz_start[i] = so[j];
+                const uint64_t sp = so[j] + pad;
+                const uint64_t r = sp <= pad ? 0 : (sp + kRun - 1) / kRun;
+                if (r < nruns) atomicMax(marks + r, (uint32_t)i);
+            }
+        }
+        __syncthreads();  // s_tile / s_wsum / s_wbase reuse
+    }
+}
+
+// Layout of the sparsified list (kept edges at `pad`): s_off, nz_*, run map.
+// Asynchronous (the non-empty count stays on the device: the edge kernel
+// reads the run_i[nruns] sentinel instead).
+static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint64_t* wpref,
+                                uint64_t* s_off, uint64_t pad, uint64_t kept, ListMeta& meta) {
+    meta.pad = pad;
+    meta.e = kept;
+    meta.ntasks = kept ? (pad + kept + kChunkEdges - 1) / kChunkEdges : 0;
+    meta.nruns = meta.ntasks * kWarp;
+    meta.nz = 0;  // on the device only
+    meta.nz_vid = g.ws.get<uint32_t>("sp.nz_vid", g.nloc + 1);
+    meta.nz_start = g.ws.get<uint64_t>("sp.nz_start", g.nloc + 1);
+    uint32_t* marks = g.ws.get<uint32_t>("sp.runmark", meta.nruns + 1);
+    meta.run_i = g.ws.get<uint32_t>("sp.run_i", meta.nruns + 1);
+    if (meta.nruns) GGB_CUDA(cudaMemsetAsync(marks, 0, meta.nruns * 4, g.stream));
+    const uint64_t ntiles = (g.nloc + 1 + kLayoutTile - 1) / kLayoutTile;
+    auto* tstate = g.ws.get<unsigned long long>("sp.tstate", ntiles + 1);
+    auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
+    GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
+    static int per_sm = 0;
+    if (!per_sm) per_sm = occupancy_grid((const void*)sp_layout_kernel, 256, 0, 1);
+    const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)per_sm * g.num_sms);
+    sp_layout_kernel<<<gr, 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref, pad, meta.nruns, s_off,
+                                               meta.nz_vid, meta.nz_start, marks, meta.run_i,
+                                               tstate, ticket, ntiles);
+    GGB_CUDA(cudaGetLastError());
+    if (!meta.nruns) return;
+    size_t tmp = 0;
+    GGB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp, marks, meta.run_i, MaxU32{}, meta.nruns,
+                                            g.stream));
+    void* tmpp = g.ws.get("cub.tmp.sp.runs", tmp);
+    GGB_CUDA(cub::DeviceScan::InclusiveScan(tmpp, tmp, marks, meta.run_i, MaxU32{}, meta.nruns,
+                                            g.stream));
+}
+
 uint64_t sparse_pad(DevGraph& g, uint64_t kept_local) {
     if (g.nranks <= 1) return 0;
     return exchange_exclusive_base(g, kept_local) % kChunkEdges;
@@ -435,14 +559,11 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
         // one pass: (sparsify +) scan + compaction at pad 0
         if (hash) launch_scan_compact<true>(g, bitmap, *hash, wpref, s_src, s_w);
         else launch_scan_compact<false>(g, bitmap, SparsifySpec{}, wpref, s_src, s_w);
-        soff_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref,
-                                                                      s_off);
-        GGB_CUDA(cudaGetLastError());
         GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
         GGB_CUDA(cudaStreamSynchronize(g.stream));
-        build_runs(g, s_off, 0, kept, "sp", meta);
+        build_sparse_layout(g, bitmap, wpref, s_off, 0, kept, meta);
         if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-        if (launches) *launches += 6;
+        if (launches) *launches += 3;
         return kept;
     }
     // several ranks: the list's padded base needs the kept counts of all
@@ -460,9 +581,6 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
     GGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, wpref, nwords + 1, g.stream));
     void* tmpp = g.ws.get("cub.tmp.rb", tmp);
     GGB_CUDA(cub::DeviceScan::ExclusiveSum(tmpp, tmp, cnt, wpref, nwords + 1, g.stream));
-    soff_kernel<<<grid_for(g.nloc + 1, 256), 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref,
-                                                                  s_off);
-    GGB_CUDA(cudaGetLastError());
     GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     const uint64_t pad = sparse_pad(g, kept);
@@ -480,9 +598,9 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
                                                         wpref, s_src, s_w, pad);
         GGB_CUDA(cudaGetLastError());
     }
-    build_runs(g, s_off, pad, kept, "sp", meta);
+    build_sparse_layout(g, bitmap, wpref, s_off, pad, kept, meta);
     if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-    if (launches) *launches += 7;
+    if (launches) *launches += 5;
     return kept;
 }
 

@@ -285,7 +285,6 @@ struct Engine {
             ea.e_end = L.e_end();
             ea.ntasks = L.ntasks;
             ea.nruns = L.nruns;
-            ea.nz = L.nz;
             ea.a_off = a_off;
             ea.st_cur = st[cu];
             ea.msg_cur = msg[cu];

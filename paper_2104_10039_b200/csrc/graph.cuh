@@ -79,8 +79,9 @@ struct ListMeta {
     uint64_t e = 0;        // local edges
     uint64_t nruns = 0;    // ntasks * 32 (every run index of a task is addressable)
     uint64_t ntasks = 0;
-    uint64_t nz = 0;       // non-empty vertices
-    uint32_t* run_i = nullptr;     // [nruns] index into nz_* of the vertex at the run's first position
+    uint64_t nz = 0;       // non-empty vertices (full list; the sparsified list keeps it on the device)
+    uint32_t* run_i = nullptr;     // [nruns+1] index into nz_* of the vertex at the run's first
+                                   // position; run_i[nruns] = nz - 1
     uint32_t* nz_vid = nullptr;    // [nz] local vertex id
     uint64_t* nz_start = nullptr;  // [nz+1] local edge offset (nz_start[nz] = e)
     uint64_t e_end() const { return pad + e; }

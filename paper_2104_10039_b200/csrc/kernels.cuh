@@ -94,7 +94,7 @@ struct EdgeArgs {
     const uint32_t* __restrict__ nz_vid;    // [nz] local vertex id
     const uint64_t* __restrict__ nz_start;  // [nz+1] local edge offset
     uint64_t pad, e_end;                    // valid padded positions [pad, e_end)
-    uint64_t ntasks, nruns, nz;
+    uint64_t ntasks, nruns;
     const uint64_t* __restrict__ a_off;     // active_in_degree offsets (engine.hpp:154-161)
     const uint8_t* __restrict__ st_cur;
     const typename P::Message* __restrict__ msg_cur;  // global ids
@@ -368,7 +368,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         }
     }
     const uint64_t rn = (t + 1) * kWarp;
-    const uint32_t i_next = rn < a.nruns ? a.run_i[rn] : (uint32_t)(a.nz - 1);
+    const uint32_t i_next = a.run_i[rn];  // run_i[nruns] = nz - 1 (sentinel)
     const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
     for (uint32_t j = lane; j < cnt; j += kWarp) {
         const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
