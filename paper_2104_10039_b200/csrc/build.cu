@@ -55,21 +55,25 @@ static inline unsigned grid_for(uint64_t n, int block, uint64_t cap = 148ull * 6
 // needs only the high word of the final mix: h_hi = x_hi ^ (x_hi >> 31) of
 // the last product x, whose high word is three 32-bit multiplies; the low
 // word is computed only when h_hi ties T's high word.
-__device__ __forceinline__ bool keep_edge(uint64_t x, uint64_t T) {
+// High word of mix64's last product for x (the part the test needs).
+__device__ __forceinline__ uint32_t mix_hi(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
     const uint64_t y = x ^ (x >> 27);
     const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
     constexpr uint32_t c_lo = 0x133111ebu, c_hi = 0x94d049bbu;  // 0x94d049bb133111eb
     const uint32_t xhi = __umulhi(ylo, c_lo) + ylo * c_hi + yhi * c_lo;
-    const uint32_t hhi = xhi ^ (xhi >> 31);
-    const uint32_t Thi = (uint32_t)(T >> 32);
+    return xhi ^ (xhi >> 31);
+}
+__device__ __forceinline__ bool keep_edge(uint64_t x, uint64_t T) {
+    const uint32_t hhi = mix_hi(x), Thi = (uint32_t)(T >> 32);
     if (hhi != Thi) return hhi < Thi;
-    const uint64_t xf = y * 0x94d049bb133111ebull;  // tie on the high word (rare)
-    return (xf ^ (xf >> 31)) < T;
+    return mix64(x) < T;  // tie on the high word (rare)
 }
 
 // Flags of bitmap word i (engine.cpp:63-75); e_base = global id of local edge 0.
+// The aligned full-word path decides all 32 edges on the high words without
+// branches and resolves high-word ties (probability ~2^-32 each) afterwards.
 __device__ __forceinline__ uint32_t sparsify_word(uint64_t i, uint64_t e_loc, uint64_t e_base,
                                                   uint64_t T, uint64_t key, int keep_all) {
     const uint64_t e0 = i * 32;
@@ -79,8 +83,19 @@ __device__ __forceinline__ uint32_t sparsify_word(uint64_t i, uint64_t e_loc, ui
         word = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
     } else if (nb == 32 && (e_base & 31) == 0) {  // key ^ (base | b) = (key ^ base) ^ b
         const uint64_t k0 = key ^ (e_base + e0);
+        const uint32_t Thi = (uint32_t)(T >> 32);
+        uint32_t tie = 0;
 #pragma unroll 8
-        for (int b = 0; b < 32; ++b) word |= (keep_edge(k0 ^ (uint64_t)b, T) ? 1u : 0u) << b;
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t h = mix_hi(k0 ^ (uint64_t)b);
+            word |= (h < Thi ? 1u : 0u) << b;
+            tie |= (h == Thi ? 1u : 0u) << b;
+        }
+        while (tie) {
+            const int b = __ffs(tie) - 1;
+            tie &= tie - 1;
+            if (mix64(k0 ^ (uint64_t)b) < T) word |= 1u << b;
+        }
     } else {
         for (int b = 0; b < nb; ++b) word |= (keep_edge(key ^ (e_base + e0 + b), T) ? 1u : 0u) << b;
     }
