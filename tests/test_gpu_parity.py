@@ -6,7 +6,7 @@ configs' shapes (reduced scale where the oracle must finish in seconds)."""
 import numpy as np
 import pytest
 
-from oracle.oracle import BP, BP_EDGE, GG, PR, SSSP, WCC, Oracle
+from oracle.oracle import BP, BP_EDGE, CSC, GG, PR, SSSP, WCC, Oracle
 from tests.parity import compare, to_graph
 
 pytestmark = pytest.mark.gpu
@@ -334,3 +334,45 @@ def test_device_sparsify_matches_reference_hash(ggb):  # engine.cpp:63-75, test_
     assert int(ggb.sparsify(e, 1.0, 9).sum()) == e and int(ggb.sparsify(e, 0.0, 9).sum()) == 0
     lo, hi = ggb.sparsify(2000, 0.3, 5), ggb.sparsify(2000, 0.7, 5)
     assert np.all(hi[lo == 1] == 1)
+
+
+# --------------------------------------------------------------------------
+# list-build tile boundaries: the one-pass scan/compaction works on tiles of
+# 1024 bitmap words (32768 edges) and the list layout on tiles of 1024
+# vertices; edge and vertex counts straddle those boundaries (empty
+# vertices, a hub spanning several 512-edge tasks, duplicate edges)
+# --------------------------------------------------------------------------
+def _exact_graph(n, e, seed, weighted=False):
+    rng = np.random.default_rng(seed)
+    p = rng.pareto(1.2, n) + 0.05
+    p[rng.random(n) < 0.25] = 0.0  # empty vertices
+    p[n // 3] = p.sum()            # one hub
+    deg = rng.multinomial(e, p / p.sum())
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(deg)
+    src = rng.integers(0, n, e).astype(np.uint32)
+    for v in range(n):  # CSC order: sources ascending per destination
+        a, b = int(off[v]), int(off[v + 1])
+        src[a:b].sort()
+    w = rng.integers(1, 50, e).astype(np.float64) if weighted else None
+    return CSC(n, off, src, w)
+
+
+@pytest.mark.parametrize("n,e", [(1023, 32767), (1024, 32768), (1025, 32769),
+                                 (2049, 3 * 32768 + 5), (5000, 98303)])
+def test_list_build_tile_boundaries(ggb, n, e):
+    g = _exact_graph(n, e, n + e)
+    gw = _exact_graph(n, e, n + e + 1, weighted=True)
+    total = 0
+    # theta is not of the form 1/k: duplicate sources make PR influences
+    # exactly 1/k, and on such an exact tie the run-granular re-association
+    # of the PR fold may round to the other side of theta (the allowed
+    # near-threshold deviation; theta = 0.05 flips one edge of 98309 here)
+    for scheme in ("sp", "gg", "sms"):
+        kw = dict(scheme=scheme, sigma=0.5, theta=0.0437, alpha=2, max_iterations=12, seed=e)
+        total += compare(ggb, g, PR, **kw)[2]
+        total += compare(ggb, g, WCC, **kw)[2]
+        total += compare(ggb, gw, SSSP, graded=True, **kw)[2]  # f64 weights
+        total += compare(ggb, gw, SSSP, graded=True,
+                         device_weights=gw.w.astype(np.float32), **kw)[2]  # f32 weights
+    assert total == 0
