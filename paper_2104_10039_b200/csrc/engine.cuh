@@ -199,7 +199,8 @@ struct Engine {
         Acc* tv = ws.get<Acc>("tv", ntask_cap);
         // superstep chain (kEdgeChain): per-task slots + the task ticket,
         // cleared before each superstep
-        constexpr size_t kSlot = chain_packed<Acc>() ? sizeof(ulonglong2) : sizeof(uint32_t);
+        constexpr size_t kSlot =
+            chain_packed<Acc>() ? sizeof(ulonglong2) * chain_halves<Acc>() : sizeof(uint32_t);
         char* chain = nullptr;
         if (cfg.scheme == GG_SCHEME_SMS || cfg.scheme == GG_SCHEME_GG)
             chain = static_cast<char*>(ws.get("chain", ntask_cap * kSlot + 16));

@@ -259,25 +259,41 @@ __device__ __forceinline__ void warp_write_flags(uint32_t* __restrict__ bitmap, 
 // (ticket), so every task looked at is held by a running warp that never
 // waits on a later task: the look-back always completes.
 //
-// Accumulators of <= 8 bytes travel with their state in one 16-byte slot
-// (one relaxed vector store / load, no fence); larger ones are written to
-// hv / tv and published by a release store of the state.
+// Accumulators of up to 32 bytes travel with their state in H = size/8
+// 16-byte halves {state, 8 value bytes}, each written and read with one
+// relaxed vector access (single-copy atomic), so no fence is needed; a slot
+// is ready when all its halves carry the same non-zero state (a reader that
+// catches a piece -> inclusive rewrite half way sees mixed states and
+// retries). Larger accumulators are written to hv / tv and published by a
+// release store of the state.
 template <class Accum>
-__host__ __device__ constexpr bool chain_packed() { return sizeof(Accum) <= 8; }
+__host__ __device__ constexpr int chain_halves() { return (int)((sizeof(Accum) + 7) / 8); }
+template <class Accum>
+__host__ __device__ constexpr bool chain_packed() { return sizeof(Accum) <= 32; }
 
 template <class Accum>
 __device__ __forceinline__ void chain_put(ulonglong2* d, uint32_t state, const Accum& v) {
-    unsigned long long bits = 0;
-    memcpy(&bits, &v, sizeof(Accum));
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};"
-                 :: "l"(d), "l"((unsigned long long)state), "l"(bits) : "memory");
+    constexpr int H = chain_halves<Accum>();
+    unsigned long long bits[H] = {};
+    memcpy(bits, &v, sizeof(Accum));
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};"
+                     :: "l"(d + h), "l"((unsigned long long)state), "l"(bits[h]) : "memory");
 }
 template <class Accum>
 __device__ __forceinline__ uint32_t chain_get(const ulonglong2* d, Accum& v) {
-    unsigned long long st, bits;
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(st), "=l"(bits) : "l"(d) : "memory");
-    memcpy(&v, &bits, sizeof(Accum));
-    return (uint32_t)st;
+    constexpr int H = chain_halves<Accum>();
+    unsigned long long st[H], bits[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(st[h]), "=l"(bits[h]) : "l"(d + h) : "memory");
+    memcpy(&v, bits, sizeof(Accum));
+    bool same = true;
+#pragma unroll
+    for (int h = 1; h < H; ++h) same = same && st[h] == st[0];
+    return same ? (uint32_t)st[0] : 0u;
 }
 
 template <class P, class W>
@@ -291,7 +307,7 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
         const int64_t j = base - lane;
         uint32_t s = kChainIncl;
         if (j >= 0) {
-            if constexpr (kPacked) s = chain_get(a.cdesc + j, v);
+            if constexpr (kPacked) s = chain_get(a.cdesc + j * chain_halves<Accum>(), v);
             else s = ld_acquire(a.chain + j);
         }
         const uint32_t incl = __ballot_sync(0xffffffffu, s == kChainIncl);
@@ -319,7 +335,9 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
         const int64_t j = wb - lane;
         uint32_t s;
         if constexpr (kPacked) {
-            s = chain_get(a.cdesc + j, v);
+            do {  // published; a multi-half slot caught mid-rewrite reads 0
+                s = chain_get(a.cdesc + j * chain_halves<Accum>(), v);
+            } while (__any_sync(0xffffffffu, s == 0));
         } else {
             s = ld_acquire(a.chain + j);
             __syncwarp();
@@ -474,7 +492,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             if (CHAIN && cont_after) {  // publish for the tasks this vertex continues into
                 const uint32_t state = first_cont ? kChainPiece : kChainIncl;
                 if constexpr (chain_packed<Accum>()) {
-                    chain_put(a.cdesc + t, state, S);
+                    chain_put(a.cdesc + t * chain_halves<Accum>(), state, S);
                 } else {
                     __threadfence();
                     st_release(a.chain + t, state);
@@ -490,7 +508,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             const Accum inc = a.prog.combine(carry, S);
             a.tv[t] = inc;
             if constexpr (chain_packed<Accum>()) {
-                chain_put(a.cdesc + t, kChainIncl, inc);
+                chain_put(a.cdesc + t * chain_halves<Accum>(), kChainIncl, inc);
             } else {
                 __threadfence();
                 st_release(a.chain + t, kChainIncl);
