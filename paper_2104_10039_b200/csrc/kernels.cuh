@@ -355,6 +355,9 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
     return acc;
 }
 
+#ifndef GGB_SHIFT_GROUP
+#define GGB_SHIFT_GROUP 8
+#endif
 template <class P, class W, int MODE, bool HOT = false>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint8_t* sp0,
                                           uint64_t t, int lane, uint64_t pol_stream,
@@ -450,13 +453,19 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     constexpr bool kShift = fold_unroll<P>() == 1 && !CHAIN &&
                             sizeof(Message) <= 16;  // larger runs stay in local memory
     if constexpr (kShift) {
+        // GGB_SHIFT_GROUP positions folded per step (inlined copies), then the
+        // run shifts down by the group: 16/G shifts of 16-G elements instead
+        // of 16 shifts of 15 (c4 approximate gather 2.27 -> 2.07 ms with G = 8;
+        // G = 16, the fully unrolled fold, measured 2.48 ms)
+        constexpr int G = GGB_SHIFT_GROUP;
 #pragma unroll 1
-        for (int j = 0; j < kRun; ++j) {
-            fold_step(j, m[0], wv(0));
+        for (int j0 = 0; j0 < kRun; j0 += G) {
 #pragma unroll
-            for (int i = 0; i + 1 < kRun; ++i) {
-                m[i] = m[i + 1];
-                if constexpr (!std::is_void_v<W>) wr[i] = wr[i + 1];
+            for (int g = 0; g < G; ++g) fold_step(j0 + g, m[g], wv(g));
+#pragma unroll
+            for (int i = 0; i + G < kRun; ++i) {
+                m[i] = m[i + G];
+                if constexpr (!std::is_void_v<W>) wr[i] = wr[i + G];
             }
         }
     } else {
