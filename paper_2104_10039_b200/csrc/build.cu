@@ -307,10 +307,9 @@ __device__ __forceinline__ uint64_t tile_lookback(unsigned long long* tstate, ui
     return excl;
 }
 
-// Held to 6 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8): the hash
-// variant is issue-bound and needs the warps (c5: 5.66 -> 4.69 ms).
+// Held to 4 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8).
 template <int WB, bool HASH>
-__global__ void __launch_bounds__(kScanThreads, WB == 0 ? 6 : WB == 4 ? 4 : 3)
+__global__ void __launch_bounds__(kScanThreads, WB == 0 ? 4 : WB == 4 ? 4 : 3)
 scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w, uint64_t e_loc,
                     uint64_t in_pad, uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_base,
                     SparsifySpec h, uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
@@ -331,8 +330,14 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
         const uint64_t w0 = t * kScanTile + (uint64_t)warp * kScanWarpWords;
         // sources of 8 words (lane l: edge l of each), loaded one batch ahead;
         // the first batch before the flags and the look-back
-        uint32_t sv[2][8];
-        WT wv[2][8];
+        // batches in registers: unweighted lists keep three batches in
+        // flight ahead of the one being stored (64 registers, 4 CTAs per SM:
+        // c5 compaction 2.35 -> 2.18 ms, sparsify + compaction 4.63 -> 4.40
+        // ms; one ahead at 6 CTAs, two at 5 and 6, four at 4 and five at 3
+        // measured slower)
+        constexpr int D = WB == 0 ? 4 : 2;
+        uint32_t sv[D][8];
+        WT wv[D][8];
         auto load_batch = [&](int k0, uint32_t (&s8)[8], WT (&w8)[8]) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -342,7 +347,8 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 if constexpr (WB != 0) w8[k] = ine ? __ldg(static_cast<const WT*>(w) + in_pad + e) : WT(0);
             }
         };
-        load_batch(0, sv[0], wv[0]);
+#pragma unroll
+        for (int b = 0; b < D - 1; ++b) load_batch(8 * b, sv[b], wv[b]);
         uint32_t word[kScanWPL], off[kScanWPL];  // off: exclusive popcount within the warp
         uint32_t run = 0;
 #pragma unroll
@@ -389,7 +395,8 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
 #pragma unroll
         for (int b = 0; b < kScanWarpWords / 8; ++b) {
             if (w0 + 8 * b >= nwords) break;
-            if (b + 1 < kScanWarpWords / 8) load_batch(8 * (b + 1), sv[(b + 1) & 1], wv[(b + 1) & 1]);
+            if (b + D - 1 < kScanWarpWords / 8)
+                load_batch(8 * (b + D - 1), sv[(b + D - 1) % D], wv[(b + D - 1) % D]);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int kw = 8 * b + k;  // word of the warp: lane kw % 32 of word[kw / 32]
@@ -397,8 +404,8 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 const uint32_t ok = __shfl_sync(0xffffffffu, off[kw / 32], kw % 32);
                 if ((wk >> lane) & 1u) {
                     const uint64_t pos = wbase + ok + (uint32_t)__popc(wk & lt);
-                    s_src[pos] = sv[b & 1][k];
-                    if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[b & 1][k];
+                    s_src[pos] = sv[b % D][k];
+                    if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[b % D][k];
                 }
             }
         }
