@@ -338,7 +338,7 @@ def test_device_sparsify_matches_reference_hash(ggb):  # engine.cpp:63-75, test_
 
 # --------------------------------------------------------------------------
 # list-build tile boundaries: the one-pass scan/compaction works on tiles of
-# 1024 bitmap words (32768 edges) and the list layout on tiles of 1024
+# 1024 bitmap words (32768 edges) and the list layout on tiles of 2048
 # vertices; edge and vertex counts straddle those boundaries (empty
 # vertices, a hub spanning several 512-edge tasks, duplicate edges)
 # --------------------------------------------------------------------------
@@ -358,8 +358,8 @@ def _exact_graph(n, e, seed, weighted=False):
     return CSC(n, off, src, w)
 
 
-@pytest.mark.parametrize("n,e", [(1023, 32767), (1024, 32768), (1025, 32769),
-                                 (2049, 3 * 32768 + 5), (5000, 98303)])
+@pytest.mark.parametrize("n,e", [(1023, 32767), (1024, 32768), (1025, 32769), (2047, 65537),
+                                 (2048, 65536), (2049, 3 * 32768 + 5), (5000, 98303)])
 def test_list_build_tile_boundaries(ggb, n, e):
     g = _exact_graph(n, e, n + e)
     gw = _exact_graph(n, e, n + e + 1, weighted=True)
