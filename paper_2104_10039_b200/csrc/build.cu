@@ -422,12 +422,12 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
     GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
     const size_t wb = weight_size(g.wkind);
-    const void* k = wb == 0 ? (const void*)scan_compact_kernel<0, HASH>
-                  : wb == 4 ? (const void*)scan_compact_kernel<4, HASH>
-                            : (const void*)scan_compact_kernel<8, HASH>;
-    static int per_sm[2][3] = {};
-    int& ps = per_sm[HASH][wb == 0 ? 0 : wb == 4 ? 1 : 2];
-    if (!ps) ps = occupancy_grid(k, kScanThreads, 0, 1);
+    // resident CTAs per SM of each instantiation (thread-safe one-time init)
+    auto per_sm = [](const void* k) { return occupancy_grid(k, kScanThreads, 0, 1); };
+    static const int ps0 = per_sm((const void*)scan_compact_kernel<0, HASH>);
+    static const int ps4 = per_sm((const void*)scan_compact_kernel<4, HASH>);
+    static const int ps8 = per_sm((const void*)scan_compact_kernel<8, HASH>);
+    const int ps = wb == 0 ? ps0 : wb == 4 ? ps4 : ps8;
     const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)ps * g.num_sms);
     if (wb == 0)
         scan_compact_kernel<0, HASH><<<gr, kScanThreads, 0, g.stream>>>(
@@ -549,8 +549,7 @@ static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint6
     auto* tstate = g.ws.get<unsigned long long>("sp.tstate", ntiles + 1);
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
     GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
-    static int per_sm = 0;
-    if (!per_sm) per_sm = occupancy_grid((const void*)sp_layout_kernel, 256, 0, 1);
+    static const int per_sm = occupancy_grid((const void*)sp_layout_kernel, 256, 0, 1);
     const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)per_sm * g.num_sms);
     sp_layout_kernel<<<gr, 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref, pad, meta.nruns, s_off,
                                                meta.nz_vid, meta.nz_start, marks, meta.run_i,

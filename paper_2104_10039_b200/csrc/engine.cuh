@@ -97,9 +97,8 @@ struct Engine {
 
     template <int MODE>
     static int grid_edge(DevGraph& g) {
-        static int cached = 0;
-        if (!cached) cached = occupancy_grid((const void*)edge_kernel<P, W, MODE>, kBlockThreads, 0,
-                                             g.num_sms);
+        static const int cached = occupancy_grid((const void*)edge_kernel<P, W, MODE>, kBlockThreads,
+                                                 0, g.num_sms);
         return cached;
     }
     // L1+L2 evict_last prefix of the message slots (GGB_HOT_KB overrides the
@@ -142,14 +141,14 @@ struct Engine {
         return b;
     }
     static void launch_edge_hot(DevGraph& g, const EdgeArgs<P, W>& ea, uint32_t nhot) {
-        static bool attr = false;
         const size_t bytes = (size_t)nhot * sizeof(Msg);
-        if (!attr) {
+        static const bool attr = [] {  // one rank per process uses the table: its device
             GGB_CUDA(cudaFuncSetAttribute((const void*)edge_kernel_hot<P, W, kEdgePlain>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)std::max<size_t>(smem_hot_bytes(), 16)));
-            attr = true;
-        }
+            return true;
+        }();
+        (void)attr;
         edge_kernel_hot<P, W, kEdgePlain><<<g.num_sms, kHotWarps * 32, bytes, g.stream>>>(ea, nhot);
         GGB_CUDA(cudaGetLastError());
     }
@@ -162,9 +161,8 @@ struct Engine {
 
     static void launch_chain(DevGraph& g, const EdgeArgs<P, W>& ea) {
         if constexpr (chain_bounded<P, W>()) {
-            static int grid = 0;
-            if (!grid) grid = occupancy_grid((const void*)edge_chain_kernel<P, W>, kBlockThreads, 0,
-                                             g.num_sms);
+            static const int grid = occupancy_grid((const void*)edge_chain_kernel<P, W>,
+                                                   kBlockThreads, 0, g.num_sms);
             edge_chain_kernel<P, W><<<grid, kBlockThreads, 0, g.stream>>>(ea);
             GGB_CUDA(cudaGetLastError());
         } else {
