@@ -419,10 +419,14 @@ struct Engine {
 
         // final properties (engine.hpp:243)
         // owned properties (vertex order) gathered from every rank
-        Prop* final_all = ws.get<Prop>("final", n);
-        GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
-                                 cudaMemcpyDeviceToDevice, g.stream));
-        if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
+        // (one rank: the owned properties are all of them, no copy)
+        Prop* final_all = prop;
+        if (g.nranks > 1) {
+            final_all = ws.get<Prop>("final", n);
+            GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
+                                     cudaMemcpyDeviceToDevice, g.stream));
+            exchange_slices(g, final_all, sizeof(Prop));
+        }
         g.project_last = [&g, prog, final_all, n]() -> const double* {  // metrics.cu
             double* proj = g.ws.get<double>("proj", n + 1);
             export_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, final_all, n, 1, proj);
@@ -433,6 +437,9 @@ struct Engine {
         if (io.out_props && !(io.opts && io.opts->device_output)) {
             if constexpr (requires { P::kRawOutput; }) {  // WCC: uint32 labels as-is
                 GGB_CUDA(cudaMemcpyAsync(io.out_props, final_all, n * 4, cudaMemcpyDeviceToHost,
+                                         g.stream));
+            } else if constexpr (std::is_same_v<Prop, double>) {  // PR, f64 SSSP: the doubles as-is
+                GGB_CUDA(cudaMemcpyAsync(io.out_props, final_all, n * 8, cudaMemcpyDeviceToHost,
                                          g.stream));
             } else {
                 double* stage = ws.get<double>("export", n * io.out_states);
