@@ -296,8 +296,11 @@ def ours(args):
         out_buf = pinned(int(np.prod(out_shape)), out_dt).reshape(out_shape)
 
         def e2e_step():
+            # the graph is uploaded for this run (gg::run(Graph, ...)): its
+            # initial sparsification overlaps the upload on one rank
             g2 = ggb.DeviceGraph.upload(host, device=local, rank=rank, nranks=world,
-                                        exchange=exchange.handle if exchange else None)
+                                        exchange=exchange.handle if exchange else None,
+                                        for_run=cfg if world == 1 else None)
             r = ggb.run(g2, program_e2e, cfg, out=out_buf)
             g2.close()
             return r

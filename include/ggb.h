@@ -138,6 +138,16 @@ int gg_abi_version(void);
 /* Graph residency. */
 gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                               gg_dev_graph** out, gg_error* err);
+/* gg_dev_graph_create for one coming sparse-scheme run (sp / sms / gg): the
+   run's initial sparsification (engine.cpp:63-75 with this sigma and seed)
+   and the compaction of the kept edges proceed chunk by chunk while the
+   sources are still being uploaded (one rank, unweighted lists; otherwise a
+   plain create). The next gg_run_* with the same sigma and seed uses that
+   list instead of sparsifying; any run clears it. Host arrays are borrowed
+   for the call only. This is what the drop-in gg::run(Graph, ...) path uses. */
+gg_status gg_dev_graph_create_for_run(const gg_csc_view* csc, const gg_part_opts* opts,
+                                      double sigma, uint64_t seed, gg_dev_graph** out,
+                                      gg_error* err);
 gg_status gg_dev_graph_destroy(gg_dev_graph* g);
 gg_status gg_dev_graph_info(const gg_dev_graph* g, uint64_t* n, uint64_t* e,
                             uint64_t* v_begin, uint64_t* v_end, uint64_t* e_local);

@@ -60,6 +60,15 @@ class DeviceGraph {
         gg_error e{};
         check(gg_dev_graph_create(&csc, &opts, &g_, &e), e);
     }
+    // uploaded for one sparse-scheme run: its sparsification overlaps the upload
+    static DeviceGraph for_run(const gg_csc_view& csc, double sigma, std::uint64_t seed,
+                               int device = -1) {
+        DeviceGraph d;
+        gg_part_opts o{device, 0, 1, nullptr};
+        gg_error e{};
+        check(gg_dev_graph_create_for_run(&csc, &o, sigma, seed, &d.g_, &e), e);
+        return d;
+    }
     static DeviceGraph rmat(const gg_rmat_params& p, const gg_part_opts& opts) {
         DeviceGraph d;
         gg_error e{};

@@ -141,7 +141,9 @@ gg::RunReport<typename A::Property> run(const DeviceGraph&, const A&, const gg::
 // The reference signature: uploads the graph for this call.
 template <class A>
 auto run(const gg::Graph& g, const A& a, const gg::EngineConfig& cfg) {
-    const DeviceGraph dg = upload(g);
+    const DeviceGraph dg = cfg.scheme == gg::Scheme::accurate
+                               ? upload(g)
+                               : DeviceGraph::for_run(view_of(g), cfg.sigma, cfg.seed);
     return run(dg, a, cfg);
 }
 

@@ -16,7 +16,8 @@ EXPORTS = (
     "gg_status_string", "gg_abi_version", "gg_bp_priors_device", "gg_device_upload",
     "gg_device_free", "gg_device_copy", "gg_last_projection", "gg_topk_error_dev",
     "gg_relative_error_dev", "gg_stretch_error_dev", "gg_dev_graph_load", "gg_dev_graph_save",
-    "gg_dev_graph_weight_kind", "gg_dev_graph_create", "gg_dev_graph_destroy",
+    "gg_dev_graph_weight_kind", "gg_dev_graph_create", "gg_dev_graph_create_for_run",
+    "gg_dev_graph_destroy",
     "gg_dev_graph_info", "gg_dev_graph_create_rmat", "gg_dev_graph_export", "gg_bp_priors",
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
@@ -103,6 +104,8 @@ def lib():
     L.gg_status_string.argtypes = [C.c_int]
     L.gg_status_string.restype = C.c_char_p
     L.gg_dev_graph_create.argtypes = [P(CscView), P(PartOpts), P(vp), P(ErrorC)]
+    L.gg_dev_graph_create_for_run.argtypes = [P(CscView), P(PartOpts), C.c_double, C.c_uint64,
+                                              P(vp), P(ErrorC)]
     L.gg_dev_graph_create_rmat.argtypes = [P(RmatParams), P(PartOpts), P(vp), P(ErrorC)]
     L.gg_dev_graph_destroy.argtypes = [vp]
     L.gg_dev_graph_info.argtypes = [vp] + [P(C.c_uint64)] * 5

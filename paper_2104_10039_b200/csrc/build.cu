@@ -314,7 +314,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                     uint64_t in_pad, uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_base,
                     SparsifySpec h, uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
                     void* __restrict__ s_w, unsigned long long* __restrict__ tstate,
-                    uint32_t* __restrict__ ticket, uint64_t ntiles) {
+                    uint32_t* __restrict__ ticket, uint64_t tile_base, uint64_t ntiles) {
     using WT = std::conditional_t<WB == 8, unsigned long long, uint32_t>;
     constexpr int kWarps = kScanThreads / 32;
     __shared__ uint32_t s_tile;
@@ -325,7 +325,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
         __syncthreads();
-        const uint64_t t = s_tile;
+        const uint64_t t = tile_base + s_tile;  // tiles [tile_base, ntiles) of this launch
         if (t >= ntiles) break;
         const uint64_t w0 = t * kScanTile + (uint64_t)warp * kScanWarpWords;
         // sources of 8 words (lane l: edge l of each), loaded one batch ahead;
@@ -413,14 +413,22 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
     }
 }
 
+// Tiles [tile_lo, tile_hi) (tile_hi = ~0: through the last tile). Launches
+// over consecutive tile ranges continue one scan: the tile states are
+// cleared by the launch starting at tile 0, and every earlier tile is
+// complete when a later range starts (same stream).
 template <bool HASH>
 static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpec& h,
-                                uint64_t* wpref, uint32_t* s_src, void* s_w) {
+                                uint64_t* wpref, uint32_t* s_src, void* s_w, uint64_t tile_lo = 0,
+                                uint64_t tile_hi = ~0ull) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
     const uint64_t ntiles = (nwords + 1 + kScanTile - 1) / kScanTile;
+    if (tile_hi > ntiles) tile_hi = ntiles;
+    if (tile_lo >= tile_hi) return;
     auto* tstate = g.ws.get<unsigned long long>("rb.tstate", ntiles + 1);
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
-    GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
+    if (tile_lo == 0) GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
+    else GGB_CUDA(cudaMemsetAsync(ticket, 0, 4, g.stream));
     const size_t wb = weight_size(g.wkind);
     // resident CTAs per SM of each instantiation (thread-safe one-time init)
     auto per_sm = [](const void* k) { return occupancy_grid(k, kScanThreads, 0, 1); };
@@ -428,19 +436,19 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     static const int ps4 = per_sm((const void*)scan_compact_kernel<4, HASH>);
     static const int ps8 = per_sm((const void*)scan_compact_kernel<8, HASH>);
     const int ps = wb == 0 ? ps0 : wb == 4 ? ps4 : ps8;
-    const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)ps * g.num_sms);
+    const uint64_t gr = std::min<uint64_t>(tile_hi - tile_lo, (uint64_t)ps * g.num_sms);
     if (wb == 0)
         scan_compact_kernel<0, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, ntiles);
+            ticket, tile_lo, tile_hi);
     else if (wb == 4)
         scan_compact_kernel<4, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, ntiles);
+            ticket, tile_lo, tile_hi);
     else
         scan_compact_kernel<8, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, ntiles);
+            ticket, tile_lo, tile_hi);
     GGB_CUDA(cudaGetLastError());
 }
 
@@ -562,6 +570,33 @@ static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint6
     void* tmpp = g.ws.get("cub.tmp.sp.runs", tmp);
     GGB_CUDA(cub::DeviceScan::InclusiveScan(tmpp, tmp, marks, meta.run_i, MaxU32{}, meta.nruns,
                                             g.stream));
+}
+
+// Initial sparsification overlapped with the graph upload
+// (gg_dev_graph_create_for_run): the hash + compaction of the edges
+// [0, e_hi) once their sources are resident; e_hi is a multiple of the scan
+// tile (32768 edges) except for the last call (e_hi = e_loc).
+uint64_t presparse_tile_edges() { return (uint64_t)kScanTile * 32; }
+void presparse_chunk(DevGraph& g, const SparsifySpec& h, uint64_t e_lo, uint64_t e_hi) {
+    const uint64_t nwords = (g.e_loc + 31) / 32;
+    uint32_t* bitmap = g.ws.get<uint32_t>("bitmap", nwords + 1);
+    uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
+    uint32_t* s_src = g.ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
+    const uint64_t te = presparse_tile_edges();
+    const uint64_t tlo = e_lo / te;
+    const uint64_t thi = e_hi >= g.e_loc ? ~0ull : e_hi / te;
+    launch_scan_compact<true>(g, bitmap, h, wpref, s_src, nullptr, tlo, thi);
+}
+// The run side: the list layout of a pre-sparsified graph; returns kept.
+uint64_t presparse_finish(DevGraph& g, uint64_t* s_off, ListMeta& meta) {
+    const uint64_t nwords = (g.e_loc + 31) / 32;
+    uint32_t* bitmap = g.ws.get<uint32_t>("bitmap", nwords + 1);
+    uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
+    uint64_t kept = 0;
+    GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    build_sparse_layout(g, bitmap, wpref, s_off, 0, kept, meta);
+    return kept;
 }
 
 uint64_t sparse_pad(DevGraph& g, uint64_t kept_local) {

@@ -134,8 +134,9 @@ struct Upload {
     }
 };
 
-gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
-                              gg_dev_graph** out, gg_error* err) {
+static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
+                             const SparsifySpec* pre, double pre_sigma, uint64_t pre_seed,
+                             gg_dev_graph** out, gg_error* err) {
     return guarded(err, [&] {
         if (!csc || !out) throw Error(GG_INVALID_ARGUMENT, "null argument");
         if (csc->n && !csc->offsets) throw Error(GG_INVALID_ARGUMENT, "offsets is null");
@@ -182,7 +183,14 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
             GGB_CUDA(cudaMemcpyAsync(g.off, csc->offsets ? csc->offsets + g.v_begin : &zero,
                                      (g.nloc + 1) * 8, cudaMemcpyHostToDevice, up.cs));
             GGB_CUDA(cudaEventRecord(up.off, up.cs));
-            const uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
+            // the initial sparsification of the coming run rides along with the
+            // upload (one rank, unweighted list): chunks are whole scan tiles
+            const bool presp = pre && g.nranks == 1 && wb == 0 && g.e_loc;
+            uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
+            if (presp) {
+                const uint64_t te = presparse_tile_edges();
+                step = (step + te - 1) / te * te;
+            }
             for (size_t k = 0; k < up.chunk.size(); ++k) {
                 const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
                 if (e > b)
@@ -208,6 +216,12 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
                 const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
                 GGB_CUDA(cudaStreamWaitEvent(g.stream, up.chunk[k], 0));
                 relabel_sources(g, g.src + pad + b, e - b);
+                if (presp && e > b) presparse_chunk(g, *pre, b, e);
+            }
+            if (presp) {
+                g.pre_sparse = true;
+                g.pre_sigma = pre_sigma;
+                g.pre_seed = pre_seed;
             }
             GGB_CUDA(cudaStreamWaitEvent(g.stream, up.done, 0));
             GGB_CUDA(cudaStreamSynchronize(g.stream));
@@ -217,6 +231,20 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
         }
         *out = h;
     });
+}
+
+gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
+                              gg_dev_graph** out, gg_error* err) {
+    return create_impl(csc, opts, nullptr, 0.0, 0, out, err);
+}
+
+gg_status gg_dev_graph_create_for_run(const gg_csc_view* csc, const gg_part_opts* opts,
+                                      double sigma, uint64_t seed, gg_dev_graph** out,
+                                      gg_error* err) {
+    if (!(sigma >= 0.0 && sigma <= 1.0))  // the run reports the field (engine.cpp:45-61)
+        return create_impl(csc, opts, nullptr, 0.0, 0, out, err);
+    const SparsifySpec h = sparsify_spec(sigma, seed, false);
+    return create_impl(csc, opts, &h, sigma, seed, out, err);
 }
 
 gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* opts,

@@ -223,9 +223,16 @@ struct Engine {
             s_off = ws.get<uint64_t>("s_off", nloc + 1);
             s_src = ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
             s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
-            const SparsifySpec hs = sparsify_spec(cfg.sigma, cfg.seed, false);
-            kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches, &hs);
+            if (g.pre_sparse && g.pre_sigma == cfg.sigma && g.pre_seed == cfg.seed) {
+                kept = presparse_finish(g, s_off, sp);  // sparsified during the upload
+                launches += 2;
+            } else {
+                const SparsifySpec hs = sparsify_spec(cfg.sigma, cfg.seed, false);
+                kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches,
+                                      &hs);
+            }
         }
+        g.pre_sparse = false;  // one run uses it (its supersteps rewrite the bitmap)
         const uint64_t* a_off = sparse ? s_off : g.off;
         // the hottest message slots (lowest ids: hot-first layout) are pinned in
         // L2 with evict_last; with several ranks each range has its own hot

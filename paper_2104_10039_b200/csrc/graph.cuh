@@ -110,6 +110,11 @@ struct DevGraph {
     // slot range, the only messages any gather reads; exchange_slices)
     std::vector<uint64_t> gathered_slots;
     ListMeta full;
+    // gg_dev_graph_create_for_run: the bitmap / compacted sources of
+    // sparsify(sigma, seed) are already in the workspace for the next run
+    bool pre_sparse = false;
+    double pre_sigma = 0.0;
+    uint64_t pre_seed = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     Workspace ws;
@@ -178,6 +183,11 @@ SparsifySpec sparsify_spec(double sigma, uint64_t seed, bool all_ones);
 uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t* s_src,
                         void* s_w, ListMeta& meta, cudaEvent_t ev0, cudaEvent_t ev1,
                         int* launches, const SparsifySpec* hash = nullptr);
+// Initial sparsification overlapped with the upload (one rank, unweighted):
+// chunks of edges [e_lo, e_hi) as their sources land, then the run's layout.
+uint64_t presparse_tile_edges();
+void presparse_chunk(DevGraph& g, const SparsifySpec& h, uint64_t e_lo, uint64_t e_hi);
+uint64_t presparse_finish(DevGraph& g, uint64_t* s_off, ListMeta& meta);
 // padded-position base of the sparsified list of this rank (exclusive scan
 // of kept counts over ranks, modulo the task size); 0 on one GPU.
 uint64_t sparse_pad(DevGraph& g, uint64_t kept_local);

@@ -119,7 +119,11 @@ class DeviceGraph:
         self.e = int(e)
 
     @classmethod
-    def upload(cls, g: Graph, device: int = -1, rank: int = 0, nranks: int = 1, exchange=None):
+    def upload(cls, g: Graph, device: int = -1, rank: int = 0, nranks: int = 1, exchange=None,
+               for_run: "EngineConfig | None" = None):
+        """for_run: the config of the one sparse-scheme run the graph is
+        uploaded for -- its initial sparsification then overlaps the upload
+        (gg_dev_graph_create_for_run)."""
         view = L.CscView(g.n, g.num_edges(), g.in_offsets.ctypes.data,
                          g.in_sources.ctypes.data if g.num_edges() else None,
                          g.weight_kind(),
@@ -128,8 +132,17 @@ class DeviceGraph:
         opts = L.PartOpts(device, rank, nranks, exchange)
         h = C.c_void_p()
         err = L.ErrorC()
-        _raise(L.lib().gg_dev_graph_create(C.byref(view), C.byref(opts), C.byref(h), C.byref(err)),
-               err)
+        sch = None
+        if for_run is not None:
+            sch = (scheme_from_name(for_run.scheme) if isinstance(for_run.scheme, str)
+                   else Scheme(for_run.scheme))
+        if sch is not None and sch != Scheme.accurate and int(for_run.seed) >= 0:
+            rc = L.lib().gg_dev_graph_create_for_run(C.byref(view), C.byref(opts),
+                                                     float(for_run.sigma), int(for_run.seed),
+                                                     C.byref(h), C.byref(err))
+        else:
+            rc = L.lib().gg_dev_graph_create(C.byref(view), C.byref(opts), C.byref(h), C.byref(err))
+        _raise(rc, err)
         return cls(h, g.n, g.num_edges())
 
     @classmethod
@@ -379,8 +392,8 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
     program's property shape/dtype, filled instead of a fresh array."""
     ccfg = cfg.c()
     owned = None
-    if isinstance(graph, Graph):
-        dg = owned = DeviceGraph.upload(graph)
+    if isinstance(graph, Graph):  # gg::run(Graph, ...): upload for this run
+        dg = owned = DeviceGraph.upload(graph, for_run=cfg)
         n, e = graph.n, graph.num_edges()
     else:
         dg = graph

@@ -376,3 +376,27 @@ def test_list_build_tile_boundaries(ggb, n, e):
         total += compare(ggb, gw, SSSP, graded=True,
                          device_weights=gw.w.astype(np.float32), **kw)[2]  # f32 weights
     assert total == 0
+
+
+def test_upload_for_run_presparsified(ggb):
+    """gg_dev_graph_create_for_run: the sparsification done during the upload
+    is used only by a run with the same sigma and seed, and only once; other
+    runs on that graph sparsify again (results equal a plain upload's)."""
+    g = Oracle.power_law(40000, 12.0, 2.1, 7)
+    cfg = ggb.EngineConfig("gg", 0.5, 0.01, 3, 15, 11)
+    other = ggb.EngineConfig("gg", 0.5, 0.01, 3, 15, 12)
+    prog = ggb.PageRankProgram()
+    plain = ggb.DeviceGraph.upload(to_graph(ggb, g))
+    ref_cfg = ggb.run(plain, prog, cfg, want_flags=True)
+    ref_other = ggb.run(plain, prog, other, want_flags=True)
+    for first, second, r1, r2 in ((cfg, cfg, ref_cfg, ref_cfg), (other, cfg, ref_other, ref_cfg)):
+        dg = ggb.DeviceGraph.upload(to_graph(ggb, g), for_run=cfg)
+        a = ggb.run(dg, prog, first, want_flags=True)   # uses the upload's list iff same config
+        b = ggb.run(dg, prog, second, want_flags=True)  # always sparsifies itself
+        for rep, ref in ((a, r1), (b, r2)):
+            assert np.array_equal(rep.final_properties, ref.final_properties)
+            assert np.array_equal(rep.flags, ref.flags)
+            assert [r.processed_edges for r in rep.per_iteration] == \
+                   [r.processed_edges for r in ref.per_iteration]
+        dg.close()
+    plain.close()
