@@ -429,7 +429,8 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
     if (tile_lo == 0) GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
     else GGB_CUDA(cudaMemsetAsync(ticket, 0, 4, g.stream));
-    const size_t wb = weight_size(g.wkind);
+    // programs that ignore the graph's weights (PR, WCC) compact sources only
+    const size_t wb = s_w ? weight_size(g.wkind) : 0;
     // resident CTAs per SM of each instantiation (thread-safe one-time init)
     auto per_sm = [](const void* k) { return occupancy_grid(k, kScanThreads, 0, 1); };
     static const int ps0 = per_sm((const void*)scan_compact_kernel<0, HASH>);
@@ -582,10 +583,12 @@ void presparse_chunk(DevGraph& g, const SparsifySpec& h, uint64_t e_lo, uint64_t
     uint32_t* bitmap = g.ws.get<uint32_t>("bitmap", nwords + 1);
     uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
     uint32_t* s_src = g.ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
+    const size_t wsz = weight_size(g.wkind);
+    void* s_w = wsz ? g.ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
     const uint64_t te = presparse_tile_edges();
     const uint64_t tlo = e_lo / te;
     const uint64_t thi = e_hi >= g.e_loc ? ~0ull : e_hi / te;
-    launch_scan_compact<true>(g, bitmap, h, wpref, s_src, nullptr, tlo, thi);
+    launch_scan_compact<true>(g, bitmap, h, wpref, s_src, s_w, tlo, thi);
 }
 // The run side: the list layout of a pre-sparsified graph; returns kept.
 uint64_t presparse_finish(DevGraph& g, uint64_t* s_off, ListMeta& meta) {
@@ -640,7 +643,7 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
     GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     const uint64_t pad = sparse_pad(g, kept);
-    const size_t wb = weight_size(g.wkind);
+    const size_t wb = s_w ? weight_size(g.wkind) : 0;  // weights only for programs that read them
     const unsigned gr = grid_for((nwords + 7) / 8 * 32, 256, 148ull * 8);
     if (g.e_loc) {
         if (wb == 0)

@@ -184,8 +184,9 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                                      (g.nloc + 1) * 8, cudaMemcpyHostToDevice, up.cs));
             GGB_CUDA(cudaEventRecord(up.off, up.cs));
             // the initial sparsification of the coming run rides along with the
-            // upload (one rank, unweighted list): chunks are whole scan tiles
-            const bool presp = pre && g.nranks == 1 && wb == 0 && g.e_loc;
+            // upload (one rank): chunks are whole scan tiles, and a chunk's
+            // weights travel right after its sources
+            const bool presp = pre && g.nranks == 1 && g.e_loc;
             uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
             if (presp) {
                 const uint64_t te = presparse_tile_edges();
@@ -193,12 +194,18 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
             }
             for (size_t k = 0; k < up.chunk.size(); ++k) {
                 const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
-                if (e > b)
+                if (e > b) {
                     GGB_CUDA(cudaMemcpyAsync(g.src + pad + b, csc->sources + g.e_base + b, (e - b) * 4,
                                              cudaMemcpyHostToDevice, up.cs));
+                    if (presp && wb)
+                        GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + (pad + b) * wb,
+                                                 static_cast<const char*>(csc->weights) +
+                                                     (g.e_base + b) * wb,
+                                                 (e - b) * wb, cudaMemcpyHostToDevice, up.cs));
+                }
                 GGB_CUDA(cudaEventRecord(up.chunk[k], up.cs));
             }
-            if (wb && g.e_loc)
+            if (wb && g.e_loc && !presp)
                 GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
                                          static_cast<const char*>(csc->weights) + g.e_base * wb,
                                          g.e_loc * wb, cudaMemcpyHostToDevice, up.cs));

@@ -400,3 +400,17 @@ def test_upload_for_run_presparsified(ggb):
                    [r.processed_edges for r in ref.per_iteration]
         dg.close()
     plain.close()
+
+
+@pytest.mark.parametrize("scheme", ["sp", "gg"])
+def test_weight_ignoring_programs_on_weighted_graphs(ggb, scheme):
+    """PageRank and WCC ignore edge weights (algorithms.hpp:25-30, 95-101);
+    on a weighted graph the sparsified list carries sources only."""
+    g = Oracle.random_graph(3000, 40000, 5, True)
+    u = Oracle.symmetrized(g)
+    kw = dict(scheme=scheme, sigma=0.5, theta=0.0437, alpha=3, max_iterations=20, seed=9)
+    total = 0
+    for w in (g.w, g.w.astype(np.float32), g.w.astype(np.uint32)):
+        total += compare(ggb, g, PR, device_weights=w, **kw)[2]
+    total += compare(ggb, u, WCC, device_weights=u.w.astype(np.uint32), **kw)[2]
+    assert total == 0
