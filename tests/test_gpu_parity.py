@@ -404,7 +404,7 @@ def test_upload_for_run_presparsified(ggb):
 
 @pytest.mark.parametrize("scheme", ["sp", "gg"])
 def test_weight_ignoring_programs_on_weighted_graphs(ggb, scheme):
-    """PageRank and WCC ignore edge weights (algorithms.hpp:25-30, 95-101);
+    """PageRank, WCC and S-state BP ignore edge weights (algorithms.hpp:15-145);
     on a weighted graph the sparsified list carries sources only."""
     g = Oracle.random_graph(3000, 40000, 5, True)
     u = Oracle.symmetrized(g)
@@ -413,4 +413,5 @@ def test_weight_ignoring_programs_on_weighted_graphs(ggb, scheme):
     for w in (g.w, g.w.astype(np.float32), g.w.astype(np.uint32)):
         total += compare(ggb, g, PR, device_weights=w, **kw)[2]
     total += compare(ggb, u, WCC, device_weights=u.w.astype(np.uint32), **kw)[2]
+    total += compare(ggb, g, BP, device_weights=g.w, **kw)[2]  # S-state BP ignores weights too
     assert total == 0
