@@ -85,11 +85,12 @@ CASES = [  # prog, scale, edge factor, seed, symmetrise, weights, theta
     ("sssp", 15, 16, 4, False, "u32", 0.05),
     ("wcc", 14, 16, 5, True, None, 0.0),
     ("bp", 14, 16, 6, False, "coupling", 0.01),
+    ("pr", 14, 16, 8, False, "u32", 0.01),  # a program that ignores the graph's weights
 ]
 
 
 @pytest.mark.parametrize("nranks", [2, 3])
-@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] + ("-" + c[5] if c[5] else "") for c in CASES])
 def test_ranks_bit_identical_to_one_gpu(ggb, case, nranks):
     prog, scale, ef, seed, sym, weights, theta = case
     graph = _graph(ggb, scale, ef, seed, sym, weights)
