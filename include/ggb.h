@@ -141,8 +141,8 @@ gg_status gg_dev_graph_create(const gg_csc_view* csc, const gg_part_opts* opts,
 /* gg_dev_graph_create for one coming sparse-scheme run (sp / sms / gg): the
    run's initial sparsification (engine.cpp:63-75 with this sigma and seed)
    and the compaction of the kept edges proceed chunk by chunk while the
-   sources are still being uploaded (one rank, unweighted lists; otherwise a
-   plain create). The next gg_run_* with the same sigma and seed uses that
+   sources are still being uploaded (one rank, at least 2^24 edges; otherwise
+   a plain create). The next gg_run_* with the same sigma and seed uses that
    list instead of sparsifying; any run clears it. Host arrays are borrowed
    for the call only. This is what the drop-in gg::run(Graph, ...) path uses. */
 gg_status gg_dev_graph_create_for_run(const gg_csc_view* csc, const gg_part_opts* opts,

@@ -184,9 +184,10 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                                      (g.nloc + 1) * 8, cudaMemcpyHostToDevice, up.cs));
             GGB_CUDA(cudaEventRecord(up.off, up.cs));
             // the initial sparsification of the coming run rides along with the
-            // upload (one rank): chunks are whole scan tiles, and a chunk's
-            // weights travel right after its sources
-            const bool presp = pre && g.nranks == 1 && g.e_loc;
+            // upload (one rank; graphs of >= 2^24 edges -- below that the extra
+            // launches cost more than the overlap saves): chunks are whole scan
+            // tiles, and a chunk's weights travel right after its sources
+            const bool presp = pre && g.nranks == 1 && g.e_loc >= (1ull << 24);
             uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
             if (presp) {
                 const uint64_t te = presparse_tile_edges();

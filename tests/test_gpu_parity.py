@@ -382,7 +382,8 @@ def test_upload_for_run_presparsified(ggb):
     """gg_dev_graph_create_for_run: the sparsification done during the upload
     is used only by a run with the same sigma and seed, and only once; other
     runs on that graph sparsify again (results equal a plain upload's)."""
-    g = Oracle.power_law(40000, 12.0, 2.1, 7)
+    g = Oracle.power_law(1500000, 12.0, 2.1, 7)  # >= 2^24 edges: the overlapped path
+    assert g.e >= 1 << 24
     cfg = ggb.EngineConfig("gg", 0.5, 0.01, 3, 15, 11)
     other = ggb.EngineConfig("gg", 0.5, 0.01, 3, 15, 12)
     prog = ggb.PageRankProgram()
