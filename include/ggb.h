@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GGB_ABI_VERSION 3
+#define GGB_ABI_VERSION 4
 
 typedef enum gg_status {
     GG_OK = 0,
@@ -54,7 +54,9 @@ typedef struct gg_csc_view {
     const uint32_t* sources;    /* e; edge id = position */
     gg_weight_kind weight_kind;
     const void* weights;        /* e elements of weight_kind, or NULL */
-    const uint32_t* out_degree; /* n, or NULL (computed on device) */
+    const uint32_t* out_degree; /* n (trusted: gg::Graph's invariant), or NULL: counted on the
+                                   host from the sources. Sources >= n and decreasing offsets
+                                   fail creation either way (checked on the device). */
 } gg_csc_view;
 
 /* Placement: one process per GPU. nranks == 1 -> single GPU. For nranks > 1
@@ -116,6 +118,8 @@ typedef struct gg_run_opts {
     uint32_t* out_flags;        /* host bitmap, ceil(e/32) words, final active-edge flags (nullable) */
     int timing;                 /* 1: CUDA-event timing of every kernel into records */
     int device_output;          /* 1: leave properties on device (out_props may be NULL) */
+    uint32_t grid_ctas;         /* test hook: cap on the CTAs of every engine launch (0 = the
+                                   occupancy-sized default); results must not depend on it */
 } gg_run_opts;
 
 /* Program parameters (algorithms.hpp). */

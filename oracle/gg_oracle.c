@@ -3,10 +3,11 @@
  *
  * Plain-C restatement of the GraphGuess reference path. Every function cites
  * the reference file:line it follows (paths relative to
- * /root/reference/proj/). Sequential on purpose: the reference's results are
- * independent of its OpenMP thread count (engine.hpp:139-140), so the
- * single-threaded fold IS the reference semantics. Only the R-MAT input
- * generator (new; not in the reference) uses OpenMP, for size.
+ * /root/reference/proj/). Each vertex's fold is sequential in CSC order; the
+ * vertex loop of an iteration (a Jacobi update) and the R-MAT input
+ * generator run over OpenMP threads. The reference's results are
+ * independent of its thread count (engine.hpp:139-140), so they are also
+ * this restatement's for any thread count.
  */
 #include "gg_oracle.h"
 
@@ -16,10 +17,11 @@
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
+#endif
+#include <stdint.h>
 
 /* largest property (bytes) the run loops keep on the stack: BP up to 32 states */
 #define OG_MAX_PSIZE 256
-#endif
 
 /* engine.cpp:9-14 (and graph.cpp:22-27, test_support.hpp:12-17) */
 uint64_t og_mix64(uint64_t x) {
@@ -633,12 +635,32 @@ static int make_prog(int which, const og_params* p, uint64_t n, int* counter, pr
 }
 
 /* ---------------------------------------------------------------------------
- * gg::run restatement — engine.hpp:141-249, sequential.
+ * gg::run restatement — engine.hpp:141-249.
+ *
+ * The vertex loop of one iteration is a Jacobi update (each vertex reads
+ * only prev[] and writes only its own next[] / status / edge flags), so it
+ * runs over OpenMP threads (cfg->threads) with each vertex's fold kept
+ * sequential in CSC order: the results are those of the reference for any
+ * thread count (engine.hpp:139-140, test_engine.cpp:161-182).
+ *
+ * Lock-step mode (og_run_ex with `ls`): in superstep s the device's flags
+ * after that superstep (ls->dev_bitmaps[s]) are compared edge by edge with
+ * the oracle's own estatus decision. An edge whose influence lies within the
+ * program's rounding band of theta (|infl - theta| <= band, see
+ * og_lockstep) and whose device flag differs is ADOPTED (counted as
+ * near-threshold), so the rest of the run follows the same flag set as the
+ * device; a differing edge outside the band is a REAL mismatch (counted,
+ * the oracle keeps its own decision).
  * ------------------------------------------------------------------------- */
-int og_run(const og_graph* g, int which, const og_params* params,
-           const og_config* cfg, void* out_props, og_record* recs,
-           uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
-           char* msg, size_t msg_cap) {
+static inline double near_band(const og_lockstep* ls, uint64_t k, double infl, double theta) {
+    const double m = fabs(infl) > theta ? fabs(infl) : theta;
+    return ls->tol_unit * ((double)(k + 4) * m + 4.0);
+}
+
+int og_run_ex(const og_graph* g, int which, const og_params* params,
+              const og_config* cfg, void* out_props, og_record* recs,
+              uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
+              char* msg, size_t msg_cap, og_lockstep* ls) {
     memset(sum, 0, sizeof(*sum));
     int rc = og_validate(cfg, msg, msg_cap);                       /* :145 */
     if (rc) return rc;
@@ -651,12 +673,22 @@ int og_run(const og_graph* g, int which, const og_params* params,
     if (make_prog(which, params, n, &counter, &P)) return fail_msg(msg, msg_cap, "bad program parameters");
     if (which == OG_BP_EDGE && !g->w) return fail_msg(msg, msg_cap, "bp_edge needs coupling weights");
     const size_t ps = P.psize;
+#ifdef _OPENMP
+    const int T = which == OG_POISON ? 1 : (int)(cfg->threads ? cfg->threads : 1);
+#endif
+    if (ls && ls->stats) memset(ls->stats, 0, 4 * ls->stats_cap * sizeof(uint64_t));
 
     uint8_t* flags = (uint8_t*)xmalloc(g->e + 1);                  /* :151-153 */
     if (cfg->scheme == OG_ACCURATE) memset(flags, 1, g->e);
-    else og_sparsify(g->e, cfg->sigma, cfg->seed, flags);
+    else {
+        const uint64_t key = og_mix64(cfg->seed);                  /* engine.cpp:63-75 */
+#pragma omp parallel for schedule(static) num_threads(T)
+        for (int64_t i = 0; i < (int64_t)g->e; ++i)
+            flags[i] = (double)(og_mix64(key ^ (uint64_t)i) >> 11) * 0x1.0p-53 < cfg->sigma ? 1 : 0;
+    }
     uint32_t* aid = (uint32_t*)xmalloc(n * 4);                     /* :154-161 */
-    for (uint64_t v = 0; v < n; ++v) {
+#pragma omp parallel for schedule(static) num_threads(T)
+    for (int64_t v = 0; v < (int64_t)n; ++v) {
         uint32_t c = 0;
         for (uint64_t e = g->off[v]; e < g->off[v + 1]; ++e) c += flags[e] ? 1 : 0;
         aid[v] = c;
@@ -668,45 +700,68 @@ int og_run(const og_graph* g, int which, const og_params* params,
     uint8_t* status = (uint8_t*)xmalloc(n);
     uint8_t* status_next = (uint8_t*)xcalloc(n, 1);
     memset(status, 1, n);
-    uint8_t acc[OG_MAX_PSIZE], fresh[OG_MAX_PSIZE];
+    uint64_t s_ord = 0;  /* supersteps so far */
 
     for (uint64_t t = 1; t <= cfg->max_iterations; ++t) {          /* :177 */
         const int mode = og_mode_for(cfg->scheme, t, cfg->alpha);
         const int approx = mode == OG_MODE_APPROXIMATE;
         const int superstep = mode == OG_MODE_SUPERSTEP;
+        const uint32_t* dev = (superstep && ls && s_ord < ls->n_dev) ? ls->dev_bitmaps[s_ord] : NULL;
+        uint64_t* st = (superstep && ls && ls->stats && s_ord < ls->stats_cap) ? ls->stats + 4 * s_ord : NULL;
         memcpy(next, prev, n * ps);                                /* :183-184 */
         memset(status_next, 0, n);
-        uint64_t gathered = 0, processed = 0;
+        uint64_t gathered = 0, processed = 0, n_near = 0, n_adopt = 0, n_real = 0, n_kept = 0;
         int changed = 0;
-        int64_t bad_vertex = -1;
-        for (uint64_t v = 0; v < n; ++v) {                         /* :194 */
-            if (!status[v] && aid[v] == 0) continue;               /* :196 */
-            P.identity(&P, acc);                                   /* :198 */
-            uint64_t local_edges = 0;
-            uint32_t new_active = 0;
-            for (uint64_t e = g->off[v]; e < g->off[v + 1]; ++e) { /* :202 */
-                if (approx && !flags[e]) continue;                 /* :203 */
-                const uint32_t s = g->src[e];
-                const double w = g->w ? g->w[e] : 1.0;             /* :205 */
-                const double infl = P.gather(&P, acc, prev + (uint64_t)s * ps, w, g->outdeg[s]);
-                if (superstep) {                                   /* :207-211 */
-                    const int keep = estatus(infl, cfg->theta);
-                    flags[e] = keep ? 1 : 0;
-                    new_active += keep ? 1 : 0;
+        int64_t bad_vertex = INT64_MAX;
+#pragma omp parallel num_threads(T) reduction(+ : gathered, processed, n_near, n_adopt, n_real, n_kept) \
+    reduction(| : changed) reduction(min : bad_vertex)
+        {
+            uint8_t acc[OG_MAX_PSIZE], fresh[OG_MAX_PSIZE];
+#pragma omp for schedule(dynamic, 2048)
+            for (int64_t vi = 0; vi < (int64_t)n; ++vi) {          /* :194 */
+                const uint64_t v = (uint64_t)vi;
+                if (!status[v] && aid[v] == 0) continue;           /* :196 */
+                P.identity(&P, acc);                               /* :198 */
+                uint64_t local_edges = 0;
+                uint32_t new_active = 0;
+                for (uint64_t e = g->off[v]; e < g->off[v + 1]; ++e) { /* :202 */
+                    if (approx && !flags[e]) continue;             /* :203 */
+                    const uint32_t s = g->src[e];
+                    const double w = g->w ? g->w[e] : 1.0;         /* :205 */
+                    const double infl = P.gather(&P, acc, prev + (uint64_t)s * ps, w, g->outdeg[s]);
+                    if (superstep) {                               /* :207-211 */
+                        int keep = estatus(infl, cfg->theta);
+                        if (ls) {
+                            const int near = fabs(infl - cfg->theta) <=
+                                             near_band(ls, e - g->off[v], infl, cfg->theta);
+                            n_near += near;
+                            if (dev) {
+                                const int d = (int)((dev[e >> 5] >> (e & 31)) & 1u);
+                                if (d != keep) {
+                                    if (near) { keep = d; ++n_adopt; }
+                                    else ++n_real;
+                                }
+                            }
+                        }
+                        flags[e] = keep ? 1 : 0;
+                        new_active += keep ? 1 : 0;
+                    }
+                    ++local_edges;
                 }
-                ++local_edges;
+                if (superstep) { aid[v] = new_active; n_kept += new_active; }  /* :214 */
+                P.apply(&P, (uint32_t)v, acc, prev + v * ps, fresh);   /* :216 */
+                const int active = P.vstatus(&P, prev + v * ps, fresh);
+                if (!P.valid(&P, fresh) && vi < bad_vertex) bad_vertex = vi;  /* :218 (min below) */
+                memcpy(next + v * ps, fresh, ps);
+                status_next[v] = active ? 1 : 0;
+                changed |= active ? 1 : 0;
+                gathered += local_edges;
+                ++processed;
             }
-            if (superstep) aid[v] = new_active;                    /* :214 */
-            P.apply(&P, (uint32_t)v, acc, prev + v * ps, fresh);   /* :216 */
-            const int active = P.vstatus(&P, prev + v * ps, fresh);
-            if (!P.valid(&P, fresh)) bad_vertex = (int64_t)v;      /* :218 (any; min below) */
-            memcpy(next + v * ps, fresh, ps);
-            status_next[v] = active ? 1 : 0;
-            changed |= active ? 1 : 0;
-            gathered += local_edges;
-            ++processed;
         }
-        if (bad_vertex >= 0) {                                     /* :226-233 */
+        if (st) { st[0] = n_near; st[1] = n_adopt; st[2] = n_real; st[3] = n_kept; }
+        if (superstep) ++s_ord;
+        if (bad_vertex != INT64_MAX) {                             /* :226-233 */
             for (uint64_t v = 0; v < n; ++v) {
                 if ((status[v] || aid[v] > 0) && !P.valid(&P, next + v * ps)) {
                     sum->err_iteration = t; sum->err_vertex = (uint32_t)v;
@@ -729,12 +784,54 @@ int og_run(const og_graph* g, int which, const og_params* params,
         tp = status; status = status_next; status_next = tp;
         if (!changed) break;                                       /* :240 */
     }
+    if (ls) ls->n_supersteps = s_ord;
     if (out_props) {
         if (which == OG_WCC) memcpy(out_props, prev, n * 4);
         else memcpy(out_props, prev, n * ps);
     }
     if (out_flags) memcpy(out_flags, flags, g->e);
     free(flags); free(aid); free(prev); free(next); free(status); free(status_next);
+    return OG_OK;
+}
+
+int og_run(const og_graph* g, int which, const og_params* params,
+           const og_config* cfg, void* out_props, og_record* recs,
+           uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
+           char* msg, size_t msg_cap) {
+    return og_run_ex(g, which, params, cfg, out_props, recs, rec_cap, sum, out_flags, msg,
+                     msg_cap, NULL);
+}
+
+/* Influence of every in-edge of destinations [v_begin, v_end) against the
+ * running accumulator of its vertex's full in-list (engine.hpp:198-211, the
+ * superstep fold) given prev[]; out[e - off[v_begin]]. */
+int og_influences(const og_graph* g, int which, const og_params* params, const void* prev_v,
+                  uint64_t v_begin, uint64_t v_end, int threads, double* out) {
+    int counter = 0;
+    prog P;
+    if (make_prog(which, params, g->n, &counter, &P) || which == OG_POISON) return OG_INVALID_ARGUMENT;
+    if (v_end > g->n || v_begin > v_end) return OG_INVALID_ARGUMENT;
+    const size_t ps = P.psize;
+    const uint8_t* prev = (const uint8_t*)prev_v;
+    const uint64_t base = g->off[v_begin];
+#ifdef _OPENMP
+    const int T = threads > 0 ? threads : 1;
+#else
+    (void)threads;
+#endif
+#pragma omp parallel num_threads(T)
+    {
+        uint8_t acc[OG_MAX_PSIZE];
+#pragma omp for schedule(dynamic, 2048)
+        for (int64_t vi = (int64_t)v_begin; vi < (int64_t)v_end; ++vi) {
+            P.identity(&P, acc);
+            for (uint64_t e = g->off[vi]; e < g->off[vi + 1]; ++e) {
+                const uint32_t s = g->src[e];
+                const double w = g->w ? g->w[e] : 1.0;
+                out[e - base] = P.gather(&P, acc, prev + (uint64_t)s * ps, w, g->outdeg[s]);
+            }
+        }
+    }
     return OG_OK;
 }
 

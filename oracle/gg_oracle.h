@@ -109,6 +109,34 @@ int og_run(const og_graph* g, int prog, const og_params* params,
            uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
            char* msg, size_t msg_cap);
 
+/* Lock-step comparison with the device's superstep flags (og_run_ex).
+ * An edge is NEAR-THRESHOLD when |infl - theta| <= band with
+ *   band = tol_unit * ((k + 4) * max(|infl|, theta) + 4),
+ * k = the edge's position in its vertex's in-list (the number of gathers
+ * folded before it). tol_unit is the program's rounding unit (times a
+ * safety factor): it bounds how far a re-associated prefix accumulator (the
+ * device joins 16-edge runs, engine.hpp:198-211 folds left to right) can
+ * move the influence; 0 for the min programs (SSSP, WCC), whose folds are
+ * exact under any grouping. */
+typedef struct og_lockstep {
+    const uint32_t* const* dev_bitmaps; /* [n_dev]: device flags right after superstep s (bit e of word e/32), NULL = none */
+    uint64_t n_dev;
+    double tol_unit;
+    uint64_t* stats;      /* out, 4 per superstep: near-threshold edges, adopted (device differs, near), real (device differs, not near), kept */
+    uint64_t stats_cap;   /* supersteps the stats array holds */
+    uint64_t n_supersteps; /* out: supersteps run */
+} og_lockstep;
+
+int og_run_ex(const og_graph* g, int prog, const og_params* params,
+              const og_config* cfg, void* out_props, og_record* recs,
+              uint64_t rec_cap, og_summary* sum, uint8_t* out_flags,
+              char* msg, size_t msg_cap, og_lockstep* ls);
+
+/* Per-edge influences of destinations [v_begin, v_end) folded over their
+ * full in-lists from prev (the superstep fold, engine.hpp:198-211). */
+int og_influences(const og_graph* g, int prog, const og_params* params, const void* prev,
+                  uint64_t v_begin, uint64_t v_end, int threads, double* out);
+
 /* One iteration of engine.hpp:194-224 restricted to destinations
  * [v_begin, v_end) — the per-rank step of a destination partition (used by
  * the multi-rank protocol tests). prev/next/status/status_next/aid are

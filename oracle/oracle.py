@@ -60,6 +60,12 @@ class _Summary(C.Structure):
                 ("err_iteration", C.c_uint64), ("err_vertex", C.c_uint32)]
 
 
+class _Lockstep(C.Structure):
+    _fields_ = [("dev_bitmaps", C.POINTER(C.c_void_p)), ("n_dev", C.c_uint64),
+                ("tol_unit", C.c_double), ("stats", C.POINTER(C.c_uint64)),
+                ("stats_cap", C.c_uint64), ("n_supersteps", C.c_uint64)]
+
+
 class _RefRecord(C.Structure):
     _fields_ = [("mode", C.c_int32), ("processed_edges", C.c_uint64),
                 ("active_vertices", C.c_uint64), ("wall_seconds", C.c_double)]
@@ -88,6 +94,7 @@ class CSC:
         if self.outdeg is None:
             self.outdeg = np.bincount(self.src, minlength=self.n).astype(np.uint32) \
                 if self.n else np.zeros(0, np.uint32)
+        self.outdeg = np.ascontiguousarray(self.outdeg, dtype=np.uint32)
 
     @property
     def e(self) -> int:
@@ -108,6 +115,8 @@ class Result:
     err_vertex: int = 0
     msg: str = ""
     flags: np.ndarray | None = None
+    # lock-step runs: per superstep {near, adopted, real, kept} (gg_oracle.h og_lockstep)
+    lockstep: list = field(default_factory=list)
 
 
 def _params(prog, damping=0.85, epsilon=None, source=0, graded=False, states=2,
@@ -166,6 +175,9 @@ class Oracle:
             L.og_run.argtypes = [G, C.c_int, C.POINTER(_Params), C.POINTER(_Config), C.c_void_p,
                                  C.POINTER(_Record), C.c_uint64, C.POINTER(_Summary), C.c_void_p,
                                  C.c_char_p, C.c_size_t]
+            L.og_run_ex.argtypes = L.og_run.argtypes + [C.POINTER(_Lockstep)]
+            L.og_influences.argtypes = [G, C.c_int, C.POINTER(_Params), C.c_void_p, C.c_uint64,
+                                        C.c_uint64, C.c_int, f64p]
             L.og_mix64.argtypes = [C.c_uint64]
             L.og_mix64.restype = C.c_uint64
             L.og_init_props.argtypes = [G, C.c_int, C.POINTER(_Params), C.c_void_p]
@@ -191,6 +203,16 @@ class Oracle:
         od = np.ctypeslib.as_array(g.outdeg, shape=(n,)).copy() if n else np.zeros(0, np.uint32)
         cls.lib().og_free_graph(gp)
         return CSC(n, off, src, w, od)
+
+    @classmethod
+    def _view(cls, g: CSC):
+        """An og_graph over the CSC's own arrays (no copy; the CSC must
+        outlive the returned struct)."""
+        v = _Graph(g.n, g.e, g.off.ctypes.data_as(C.POINTER(C.c_uint64)),
+                   g.src.ctypes.data_as(C.POINTER(C.c_uint32)),
+                   g.w.ctypes.data_as(C.POINTER(C.c_double)) if g.w is not None else None,
+                   g.outdeg.ctypes.data_as(C.POINTER(C.c_uint32)))
+        return v
 
     @classmethod
     def _ptr(cls, g: CSC):
@@ -280,7 +302,13 @@ class Oracle:
 
     @classmethod
     def run(cls, g: CSC, prog, scheme=ACCURATE, sigma=1.0, theta=0.0, alpha=1,
-            max_iterations=100, seed=0, threads=1, want_flags=False, **pp) -> Result:
+            max_iterations=100, seed=0, threads=1, want_flags=False, device_flags=None,
+            tol_unit=None, **pp) -> Result:
+        """og_run. Lock-step (og_run_ex) when `tol_unit` is given:
+        `device_flags` = the device's flag bitmaps (uint32 words) right
+        after each superstep, in order (None entries: no comparison); edges
+        within the near-threshold band whose device flag differs are
+        adopted, others are counted as real mismatches (Result.lockstep)."""
         L = cls.lib()
         params = _params(prog, **pp)
         cfg = _Config(scheme, sigma, theta, alpha, max_iterations, seed, threads)
@@ -291,17 +319,47 @@ class Oracle:
         props = _prop_shape(prog, g.n, pp.get("states", 2))
         flags = np.zeros(max(g.e, 1), np.uint8) if want_flags else None
         msg = C.create_string_buffer(256)
-        gp = cls._ptr(g)
-        rc = L.og_run(gp, prog, C.byref(params), C.byref(cfg), props.ctypes.data, recs, cap,
-                      C.byref(summ), flags.ctypes.data if flags is not None else None, msg, 256)
-        L.og_free_graph(gp)
+        gv = cls._view(g)
+        args = [C.byref(gv), prog, C.byref(params), C.byref(cfg), props.ctypes.data, recs, cap,
+                C.byref(summ), flags.ctypes.data if flags is not None else None, msg, 256]
+        stats_out = []
+        if tol_unit is None:
+            rc = L.og_run(*args)
+        else:
+            dev = [None if d is None else np.ascontiguousarray(d, np.uint32) for d in
+                   (device_flags or [])]
+            ptrs = (C.c_void_p * max(len(dev), 1))(*[d.ctypes.data if d is not None else None
+                                                       for d in dev])
+            scap = max(len(dev), max_iterations if max_iterations < 4096 else 4096, 1)
+            stats = np.zeros(4 * scap, np.uint64)
+            ls = _Lockstep(ptrs, len(dev), float(tol_unit),
+                           stats.ctypes.data_as(C.POINTER(C.c_uint64)), scap, 0)
+            rc = L.og_run_ex(*args, C.byref(ls))
+            for i in range(min(int(ls.n_supersteps), scap)):
+                near, adopted, real, kept = (int(x) for x in stats[4 * i:4 * i + 4])
+                stats_out.append(dict(near=near, adopted=adopted, real=real, kept=kept,
+                                      compared=i < len(dev) and dev[i] is not None))
         k = int(min(summ.iterations_run, cap))
         return Result(rc, props, [int(recs[i].mode) for i in range(k)],
                       [int(recs[i].processed_edges) for i in range(k)],
                       [int(recs[i].active_vertices) for i in range(k)], [],
                       int(summ.iterations_run), int(summ.total_processed_edges),
                       int(summ.err_iteration), int(summ.err_vertex), msg.value.decode(),
-                      flags[:g.e] if flags is not None else None)
+                      flags[:g.e] if flags is not None else None, stats_out)
+
+    @classmethod
+    def influences(cls, g: CSC, prog, prev, v_begin=0, v_end=None, threads=1, **pp):
+        """Per-edge superstep influences of destinations [v_begin, v_end)
+        from properties `prev` (og_influences)."""
+        v_end = g.n if v_end is None else v_end
+        params = _params(prog, **pp)
+        out = np.zeros(max(int(g.off[v_end] - g.off[v_begin]), 1), np.float64)
+        prev = np.ascontiguousarray(prev)
+        gv = cls._view(g)
+        if cls.lib().og_influences(C.byref(gv), prog, C.byref(params), prev.ctypes.data, v_begin,
+                                   v_end, threads, out):
+            raise ValueError("og_influences failed")
+        return out[:int(g.off[v_end] - g.off[v_begin])]
 
     # -- per-range step (multi-rank protocol tests) ----------------------------
     class Stepper:

@@ -62,8 +62,12 @@ class ErrorC(C.Structure):
     _fields_ = [("iteration", C.c_uint64), ("vertex", C.c_uint32), ("msg", C.c_char * 256)]
 
 
+ABI_VERSION = 4  # include/ggb.h GGB_ABI_VERSION
+
+
 class RunOptsC(C.Structure):
-    _fields_ = [("out_flags", C.c_void_p), ("timing", C.c_int), ("device_output", C.c_int)]
+    _fields_ = [("out_flags", C.c_void_p), ("timing", C.c_int), ("device_output", C.c_int),
+                ("grid_ctas", C.c_uint32)]
 
 
 class PrParams(C.Structure):
@@ -99,6 +103,10 @@ def lib():
     missing = [s for s in EXPORTS if not hasattr(L, s)]
     if missing:
         raise ImportError(f"libggb.so lacks symbols {missing}")
+    L.gg_abi_version.restype = C.c_int
+    if L.gg_abi_version() != ABI_VERSION:
+        raise ImportError(f"libggb.so ABI {L.gg_abi_version()} != {ABI_VERSION} (stale build: "
+                          "run __graft_entry__.build())")
     P = C.POINTER
     vp = C.c_void_p
     L.gg_status_string.argtypes = [C.c_int]

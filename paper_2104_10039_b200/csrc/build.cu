@@ -695,11 +695,34 @@ __global__ void slot_fill_kernel(const uint32_t* __restrict__ sorted_v, uint64_t
     }
 }
 
+// vertex ids -> message slots; with `bad`, sources >= n are flagged (and
+// mapped to slot 0) instead of read out of bounds
 __global__ void relabel_kernel(uint32_t* __restrict__ src, uint64_t count,
-                               const uint32_t* __restrict__ slot_of) {
+                               const uint32_t* __restrict__ slot_of, uint64_t n,
+                               unsigned int* __restrict__ bad) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        src[i] = __ldg(slot_of + src[i]);
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src[i];
+        if (bad && s >= n) {
+            *bad = 1;
+            src[i] = 0;
+        } else {
+            src[i] = __ldg(slot_of + s);
+        }
+    }
+}
+
+// local offsets must not decrease (Graph::validate, graph.cpp:83-86)
+__global__ void offsets_check_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
+                                     unsigned int* __restrict__ bad) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nloc;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        if (off[v] > off[v + 1]) *bad = 1;
+}
+void check_offsets(DevGraph& g, unsigned int* bad) {
+    if (!g.nloc) return;
+    offsets_check_kernel<<<grid_for(g.nloc, 256), 256, 0, g.stream>>>(g.off, g.nloc, bad);
+    GGB_CUDA(cudaGetLastError());
 }
 
 __global__ void gathered_count_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
@@ -757,9 +780,9 @@ void compute_slots(DevGraph& g) {
     dev_free(k0, g.stream); dev_free(k1, g.stream); dev_free(v0, g.stream); dev_free(v1, g.stream); dev_free(db, g.stream); dev_free(tmpp, g.stream);
 }
 
-void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count) {
+void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count, unsigned int* bad) {
     if (!count) return;
-    relabel_kernel<<<grid_for(count, 256), 256, 0, g.stream>>>(src, count, g.slot_of);
+    relabel_kernel<<<grid_for(count, 256), 256, 0, g.stream>>>(src, count, g.slot_of, g.n, bad);
     GGB_CUDA(cudaGetLastError());
 }
 

@@ -162,7 +162,7 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
             if (wb) g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
             g.full.pad = pad;
             std::vector<uint32_t> host_deg;
-            if (!csc->out_degree) {  // reference graphs carry it; compute for bare CSC views
+            if (!csc->out_degree) {  // reference graphs carry it; computed here for bare CSC views
                 host_deg.assign(g.n, 0);
                 for (uint64_t i = 0; i < csc->e; ++i) {
                     if (csc->sources[i] >= g.n)
@@ -170,6 +170,9 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                     ++host_deg[csc->sources[i]];
                 }
             }
+            // device-side validation flags: [0] source >= n, [1] offsets decrease
+            unsigned int* bad = g.ws.get<unsigned int>("create.bad", 4);
+            GGB_CUDA(cudaMemsetAsync(bad, 0, 16, g.stream));
             const uint32_t* deg = csc->out_degree ? csc->out_degree : host_deg.data();
             // Pipelined upload: the copy stream carries out-degrees, offsets,
             // then the sources in chunks and the weights over PCIe while the
@@ -219,11 +222,12 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                 rebase_kernel<<<256, 256, 0, g.stream>>>(g.off, g.nloc + 1, g.e_base, g.off);
                 GGB_CUDA(cudaGetLastError());
             }
+            check_offsets(g, bad + 1);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
             for (size_t k = 0; k < up.chunk.size(); ++k) {
                 const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
                 GGB_CUDA(cudaStreamWaitEvent(g.stream, up.chunk[k], 0));
-                relabel_sources(g, g.src + pad + b, e - b);
+                relabel_sources(g, g.src + pad + b, e - b, csc->out_degree ? bad : nullptr);
                 if (presp && e > b) presparse_chunk(g, *pre, b, e);
             }
             if (presp) {
@@ -232,7 +236,14 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                 g.pre_seed = pre_seed;
             }
             GGB_CUDA(cudaStreamWaitEvent(g.stream, up.done, 0));
+            unsigned int hbad[4];
+            GGB_CUDA(cudaMemcpyAsync(hbad, bad, 16, cudaMemcpyDeviceToHost, g.stream));
             GGB_CUDA(cudaStreamSynchronize(g.stream));
+            // every rank fails together (a rank that failed alone would leave
+            // the others waiting in the first exchange)
+            const uint64_t code = exchange_sum(g, (hbad[1] ? 1ull << 32 : 0ull) | (hbad[0] ? 1ull : 0ull));
+            if (code >> 32) throw Error(GG_INVALID_ARGUMENT, "graph: offsets decrease");
+            if (code & 0xffffffffull) throw Error(GG_INVALID_ARGUMENT, "edge source out of range");
         } catch (...) {
             delete h;
             throw;

@@ -95,11 +95,14 @@ struct Engine {
     using Msg = typename P::Message;
     using Acc = typename P::Accum;
 
+    // CTAs of one launch: `full` (the occupancy-sized grid) unless the run's
+    // grid_ctas test hook caps it (gg_run_opts; results do not depend on it)
+    static unsigned capped(unsigned full, unsigned cap) { return cap && cap < full ? cap : full; }
     template <int MODE>
     static int grid_edge(DevGraph& g) {
-        static const int cached = occupancy_grid((const void*)edge_kernel<P, W, MODE>, kBlockThreads,
-                                                 0, g.num_sms);
-        return cached;
+        static const int per_sm = occupancy_grid((const void*)edge_kernel<P, W, MODE>, kBlockThreads,
+                                                 0, 1);
+        return per_sm * g.num_sms;
     }
     // L1+L2 evict_last prefix of the message slots (GGB_HOT_KB overrides the
     // measured default of 24 MB for message arrays larger than L2's share)
@@ -140,33 +143,35 @@ struct Engine {
         }();
         return b;
     }
-    static void launch_edge_hot(DevGraph& g, const EdgeArgs<P, W>& ea, uint32_t nhot) {
+    static void launch_edge_hot(DevGraph& g, const EdgeArgs<P, W>& ea, uint32_t nhot, unsigned cap) {
         const size_t bytes = (size_t)nhot * sizeof(Msg);
-        static const bool attr = [] {  // one rank per process uses the table: its device
+        // the dynamic shared-memory limit is per device context: set once per device
+        static bool attr_set[64] = {};
+        if (g.device < 0 || g.device >= 64 || !attr_set[g.device]) {
             GGB_CUDA(cudaFuncSetAttribute((const void*)edge_kernel_hot<P, W, kEdgePlain>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)std::max<size_t>(smem_hot_bytes(), 16)));
-            return true;
-        }();
-        (void)attr;
-        edge_kernel_hot<P, W, kEdgePlain><<<g.num_sms, kHotWarps * 32, bytes, g.stream>>>(ea, nhot);
+            if (g.device >= 0 && g.device < 64) attr_set[g.device] = true;
+        }
+        edge_kernel_hot<P, W, kEdgePlain><<<capped(g.num_sms, cap), kHotWarps * 32, bytes, g.stream>>>(
+            ea, nhot);
         GGB_CUDA(cudaGetLastError());
     }
 
     template <int MODE>
-    static void launch_edge(DevGraph& g, const EdgeArgs<P, W>& ea) {
-        edge_kernel<P, W, MODE><<<grid_edge<MODE>(g), kBlockThreads, 0, g.stream>>>(ea);
+    static void launch_edge(DevGraph& g, const EdgeArgs<P, W>& ea, unsigned cap) {
+        edge_kernel<P, W, MODE><<<capped(grid_edge<MODE>(g), cap), kBlockThreads, 0, g.stream>>>(ea);
         GGB_CUDA(cudaGetLastError());
     }
 
-    static void launch_chain(DevGraph& g, const EdgeArgs<P, W>& ea) {
+    static void launch_chain(DevGraph& g, const EdgeArgs<P, W>& ea, unsigned cap) {
         if constexpr (chain_bounded<P, W>()) {
-            static const int grid = occupancy_grid((const void*)edge_chain_kernel<P, W>,
-                                                   kBlockThreads, 0, g.num_sms);
-            edge_chain_kernel<P, W><<<grid, kBlockThreads, 0, g.stream>>>(ea);
+            static const int per_sm = occupancy_grid((const void*)edge_chain_kernel<P, W>,
+                                                     kBlockThreads, 0, 1);
+            edge_chain_kernel<P, W><<<capped(per_sm * g.num_sms, cap), kBlockThreads, 0, g.stream>>>(ea);
             GGB_CUDA(cudaGetLastError());
         } else {
-            launch_edge<kEdgeChain>(g, ea);
+            launch_edge<kEdgeChain>(g, ea, cap);
         }
     }
 
@@ -178,6 +183,8 @@ struct Engine {
         const bool sparse = cfg.scheme != GG_SCHEME_ACCURATE;
         int launches = 0;
         Workspace& ws = g.ws;
+        g.project_last = nullptr;  // no valid run until this one completes
+        const unsigned cap = io.opts ? io.opts->grid_ctas : 0u;
 
         Msg* msg[2] = {ws.get<Msg>("msg0", n), ws.get<Msg>("msg1", n)};
         Prop* prop = ws.get<Prop>("prop", nloc + 1);
@@ -338,17 +345,17 @@ struct Engine {
                 const bool all_proc = approx || cfg.scheme == GG_SCHEME_ACCURATE;
                 if (super) {
                     GGB_CUDA(cudaMemsetAsync(chain, 0, L.ntasks * kSlot + 4, g.stream));
-                    launch_chain(g, ea);
+                    launch_chain(g, ea, cap);
                 } else if (all_proc && nhot) {
-                    if constexpr (kHotOK) launch_edge_hot(g, ea, nhot);
+                    if constexpr (kHotOK) launch_edge_hot(g, ea, nhot, cap);
                 }
-                else if (all_proc) launch_edge<kEdgePlain>(g, ea);
-                else launch_edge<kEdgeCheck>(g, ea);
+                else if (all_proc) launch_edge<kEdgePlain>(g, ea, cap);
+                else launch_edge<kEdgeCheck>(g, ea, cap);
                 ++launches;
             }
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 1), g.stream));
-            if (super) vertex_kernel<P, W, true><<<grid1d(nloc), 256, 0, g.stream>>>(va);
-            else vertex_kernel<P, W, false><<<grid1d(nloc), 256, 0, g.stream>>>(va);
+            if (super) vertex_kernel<P, W, true><<<capped(grid1d(nloc), cap), 256, 0, g.stream>>>(va);
+            else vertex_kernel<P, W, false><<<capped(grid1d(nloc), cap), 256, 0, g.stream>>>(va);
             GGB_CUDA(cudaGetLastError());
             ++launches;
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 2), g.stream));

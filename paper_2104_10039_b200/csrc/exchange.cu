@@ -155,6 +155,39 @@ uint64_t exchange_sum(DevGraph& g, uint64_t local) {
     return s;
 }
 
+__global__ void add_u32_kernel(uint32_t* __restrict__ acc, const uint32_t* __restrict__ x,
+                               uint64_t count) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        acc[i] += x[i];
+}
+
+void exchange_allreduce_u32(DevGraph& g, uint32_t* buf, uint64_t count) {
+    if (g.nranks <= 1 || !count) return;
+    if (g.exchange && g.exchange->local) {
+        LocalGroup& L = *g.exchange->local;
+        // every rank publishes a copy of its input, then sums the others' copies
+        uint32_t* mine = g.ws.get<uint32_t>("xred.mine", count);
+        uint32_t* tmp = g.ws.get<uint32_t>("xred.tmp", count);
+        GGB_CUDA(cudaMemcpyAsync(mine, buf, count * 4, cudaMemcpyDeviceToDevice, g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        L.bufs[g.rank] = mine;
+        L.barrier();
+        const unsigned grid = (unsigned)std::min<uint64_t>((count + 255) / 256, 148ull * 16);
+        for (int r = 0; r < g.nranks; ++r) {
+            if (r == g.rank) continue;
+            GGB_CUDA(cudaMemcpyAsync(tmp, L.bufs[r], count * 4, cudaMemcpyDefault, g.stream));
+            add_u32_kernel<<<grid, 256, 0, g.stream>>>(buf, tmp, count);
+            GGB_CUDA(cudaGetLastError());
+        }
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        L.barrier();  // nobody frees or rewrites its copy while another rank reads it
+        return;
+    }
+    nccl_check(nccl().AllReduce(buf, buf, count, ncclUint32, ncclSum, g.exchange->comm, g.stream),
+               "allreduce(u32)");
+}
+
 void exchange_counters(DevGraph& g, void* ctr_v) {
     if (g.nranks <= 1) return;
     if (g.exchange && g.exchange->local) {

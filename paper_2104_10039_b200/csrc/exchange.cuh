@@ -50,5 +50,8 @@ void exchange_counters(DevGraph& g, void* ctr);
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local);
 // sum of `local` over all ranks
 uint64_t exchange_sum(DevGraph& g, uint64_t local);
+// element-wise sum over ranks of a device u32[count] array, in place
+// (setup only: graph validation)
+void exchange_allreduce_u32(DevGraph& g, uint32_t* buf, uint64_t count);
 
 }  // namespace ggb

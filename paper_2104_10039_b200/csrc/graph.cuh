@@ -165,7 +165,10 @@ void assign_slots(DevGraph& g);
 // the two halves of assign_slots, for the pipelined upload: slot_of /
 // vtx_of_slot (stream-ordered, no sync) and the in-place source relabel
 void compute_slots(DevGraph& g);
-void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count);
+// (bad != nullptr: range-check the sources, flagging any >= n into *bad)
+void relabel_sources(DevGraph& g, uint32_t* src, uint64_t count, unsigned int* bad = nullptr);
+// flag decreasing local offsets into *bad (Graph::validate, graph.cpp:83-86)
+void check_offsets(DevGraph& g, unsigned int* bad);
 // Copy the full list's sources back to host as vertex ids.
 void export_sources(const DevGraph& g, uint32_t* host_out);
 // Size `meta` for (pad, e) and build its run -> vertex map from `off`.

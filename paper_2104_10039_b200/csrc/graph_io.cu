@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 
+#include "exchange.cuh"
 #include "graph.cuh"
 
 namespace ggb {
@@ -117,6 +118,14 @@ __global__ void range_kernel(const uint32_t* __restrict__ src, uint64_t count, u
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x)
         if (src[i] >= n) *bad = 1;
+}
+
+__global__ void deg_check_kernel(const uint32_t* __restrict__ counted,
+                                 const uint32_t* __restrict__ stored, uint64_t n,
+                                 unsigned int* __restrict__ bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (counted[i] != stored[i]) *bad = 1;
 }
 
 template <class T>
@@ -241,7 +250,18 @@ gg_status gg_dev_graph_load(const char* path, const gg_part_opts* opts, gg_dev_g
                     }
                     range_kernel<<<grid_n(g.e_loc), 256, 0, g.stream>>>(g.src + pad, g.e_loc, n,
                                                                          bad);
+                    // the stored out-degrees must be those of the sources
+                    // (Graph::validate, graph.cpp:88-93): count this rank's
+                    // sources, sum over ranks, compare
+                    uint32_t* cnt = static_cast<uint32_t*>(dev_alloc((n + 1) * 4, g.stream));
+                    GGB_CUDA(cudaMemsetAsync(cnt, 0, (n + 1) * 4, g.stream));
+                    count_kernel<<<grid_n(g.e_loc), 256, 0, g.stream>>>(g.src + pad, g.e_loc, n, cnt);
                     GGB_CUDA(cudaGetLastError());
+                    exchange_allreduce_u32(g, cnt, n);
+                    deg_check_kernel<<<grid_n(n), 256, 0, g.stream>>>(cnt, g.outdeg, n, bad + 1);
+                    GGB_CUDA(cudaGetLastError());
+                    GGB_CUDA(cudaStreamSynchronize(g.stream));
+                    dev_free(cnt, g.stream);
                 }
                 if (wb) {
                     const uint64_t per_w = kStage / wb;
@@ -271,6 +291,7 @@ gg_status gg_dev_graph_load(const char* path, const gg_part_opts* opts, gg_dev_g
             GGB_CUDA(cudaMemcpy(hb, bad, 16, cudaMemcpyDeviceToHost));
             dev_free(bad, g.stream);
             if (hb[0]) fail(p + ": corrupt " + fmt + " source array");
+            if (hb[1]) fail("graph: out_degree inconsistent with edges");
             if (hb[3]) fail("graph: negative or non-finite weight");
             assign_slots(g);
             build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);

@@ -336,7 +336,8 @@ class RunReport:
     total_processed_edges: int
     kept_edges: int = 0
     kernel_launches: int = 0
-    flags: np.ndarray | None = None  # final active-edge bitmap (when requested)
+    flags: np.ndarray | None = None  # final active-edge flags, one byte per edge (when requested)
+    flag_words: np.ndarray | None = None  # the same flags as the device bitmap (uint32 words)
 
 
 def validate(cfg: EngineConfig) -> None:
@@ -382,14 +383,17 @@ def _out_buffer(out, shape, dtype):
 
 
 def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: bool = False,
-        rec_cap: int | None = None, device_output: bool = False, out=None) -> RunReport:
+        rec_cap: int | None = None, device_output: bool = False, out=None,
+        grid_ctas: int = 0) -> RunReport:
     """gg::run (engine.hpp:141-249) on the device. `graph` is a Graph
     (uploaded for the call) or a DeviceGraph (already resident).
     timing: CUDA-event time of every kernel into the records.
     device_output: leave the final properties in HBM (no D2H copy;
     final_properties is then None).
     out: caller-owned result array (e.g. pinned host memory) of the
-    program's property shape/dtype, filled instead of a fresh array."""
+    program's property shape/dtype, filled instead of a fresh array.
+    grid_ctas: test hook, caps the CTAs of every engine launch (0 = the
+    occupancy-sized grid); results are identical for any value."""
     ccfg = cfg.c()
     owned = None
     if isinstance(graph, Graph):  # gg::run(Graph, ...): upload for this run
@@ -404,7 +408,7 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         summ = L.RunSummaryC()
         flags = np.zeros(max((e + 31) // 32, 1), np.uint32) if want_flags else None
         opts = L.RunOptsC(flags.ctypes.data if flags is not None else None, int(timing),
-                          int(device_output))
+                          int(device_output), int(grid_ctas))
         err = L.ErrorC()
         lib = L.lib()
         if isinstance(program, PageRankProgram):
@@ -455,7 +459,7 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         return RunReport(out_props, int(summ.iterations_run), per,
                          float(summ.total_wall_seconds), int(summ.total_processed_edges),
                          int(summ.kept_edges), int(summ.kernel_launches),
-                         unpack_bitmap(flags, e) if flags is not None else None)
+                         unpack_bitmap(flags, e) if flags is not None else None, flags)
     finally:
         if owned is not None:
             owned.close()

@@ -1,19 +1,24 @@
 """Parity at the BASELINE configs' FULL sizes (c2-c5): the device engine
-against the unmodified reference gg::run (oracle/_ref, all host threads) on
-the same R-MAT graph, generated on the device and exported.
+against the unmodified reference gg::run (oracle/_ref, all host threads)
+and the lock-step C oracle, on the same R-MAT graph (generated on the
+device and exported), over the bench's whole run (max_iterations = the
+accurate run's iterations_run, bench.cpp:173), early exit included.
 
-Per config: identical iteration count, per-iteration mode / processed_edges
-/ active_vertices (after a superstep these counts pin the kept-edge masks),
-and final properties bit-exact (SSSP u32 distances, WCC labels) or within
-the stated relative tolerance (PR 1e-9, fp32-stored BP 2e-6).
-Iteration budgets are capped so every reference run stays within tens of
-seconds; each cap still covers the first superstep (t = alpha + 1 = 5) and
-the approximate iterations on both sides of it.
+Per config:
+* masks: the device's flags right after every superstep against the
+  oracle's estatus decisions in lock-step (tests/parity.py): zero real
+  mismatches; the near-threshold edges (influence within the program's
+  rounding band of theta, decided differently by the device) are counted
+  and printed; the final masks are then identical edge for edge;
+* records: iteration count and per-iteration mode / processed_edges /
+  active_vertices identical to the reference's (to the lock-step oracle's
+  when a near-threshold edge was adopted, which changes later counts);
+* properties: bit-exact (SSSP u32 distances, WCC labels) or within the
+  stated relative tolerance (PR 1e-9, fp32-stored BP 2e-6);
+* run-to-run determinism of the device engine at full scale.
 
-c2 also checks that the device R-MAT generator reproduces the CPU
-generator (oracle/gg_oracle.c, og_rmat) at full scale; c2 and c3 (and c5 with
-GGB_FULL_MASKS=1) compare the final active-edge masks edge by edge with the C
-oracle.
+c2 also checks that the device R-MAT generator reproduces the CPU generator
+(oracle/gg_oracle.c, og_rmat) at full scale.
 """
 from __future__ import annotations
 
@@ -23,45 +28,12 @@ import numpy as np
 import pytest
 
 from oracle.oracle import GG, Oracle, Reference
+from tests.parity import NEAR_UNIT, superstep_flags
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 THREADS = os.cpu_count() or 1
 RTOL = {"pr": 1e-9, "bp": 2e-6}
-
-
-def _run_both(ggb, name, max_iterations, want_flags=False):
-    import bench
-    wl = bench.WORKLOADS[name]
-    dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],
-                              weights=wl["weights"])
-    program = bench.make_program(ggb, wl, dg, dg.n)
-    cfg = ggb.EngineConfig("gg", bench.SIGMA, wl["theta"], bench.ALPHA, max_iterations,
-                           wl["seed"])
-    rep = ggb.run(dg, program, cfg, want_flags=want_flags)
-    # run-to-run determinism at full scale: a second run is bit-identical
-    again = ggb.run(dg, program, cfg)
-    assert np.array_equal(np.asarray(again.final_properties).view(np.uint8),
-                          np.asarray(rep.final_properties).view(np.uint8))
-    assert [r.processed_edges for r in again.per_iteration] == \
-        [r.processed_edges for r in rep.per_iteration]
-    host = dg.to_host()
-    dg.close()
-    g = bench.ref_inputs(wl, host)
-    prog, pp = bench.ref_params(wl, g)
-    ref = Reference.run(g, prog, scheme=GG, sigma=bench.SIGMA, theta=wl["theta"],
-                        alpha=bench.ALPHA, max_iterations=max_iterations, seed=wl["seed"],
-                        threads=THREADS, **pp)
-    assert ref.status == 0, ref.msg
-    return wl, rep, ref, host
-
-
-def _check_records(rep, ref):
-    assert rep.iterations_run == ref.iterations_run
-    assert [int(r.mode) for r in rep.per_iteration] == ref.modes
-    assert [r.processed_edges for r in rep.per_iteration] == ref.processed_edges
-    assert [r.active_vertices for r in rep.per_iteration] == ref.active_vertices
-    assert 2 in ref.modes, "the capped budget must include a superstep"
 
 
 @pytest.fixture(scope="module")
@@ -70,27 +42,71 @@ def need_reference():
         pytest.skip("oracle/_ref/libggref.so not built")
 
 
-def _check_masks(wl, rep, host, max_iterations):
-    """Final active-edge masks against the C oracle (the reference keeps its
-    flags internal): identical, i.e. zero edges within rounding of theta."""
+def _full(ggb, name):
     import bench
+    wl = bench.WORKLOADS[name]
+    dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],
+                              weights=wl["weights"])
+    program = bench.make_program(ggb, wl, dg, dg.n)
+    acc = ggb.run(dg, program, ggb.EngineConfig("accurate", max_iterations=bench.budget_for(wl, dg.n)),
+                  device_output=True)
+    budget = acc.iterations_run
+    cfg = ggb.EngineConfig("gg", bench.SIGMA, wl["theta"], bench.ALPHA, budget, wl["seed"])
+    rep = ggb.run(dg, program, cfg, want_flags=True)
+    # run-to-run determinism at full scale: a second run is bit-identical
+    again = ggb.run(dg, program, cfg)
+    assert np.array_equal(np.asarray(again.final_properties).view(np.uint8),
+                          np.asarray(rep.final_properties).view(np.uint8))
+    assert [r.processed_edges for r in again.per_iteration] == \
+        [r.processed_edges for r in rep.per_iteration]
+    dev_flags = superstep_flags(ggb, dg, program, cfg, rep)
+    host = dg.to_host()
+    dg.close()
     g = bench.ref_inputs(wl, host)
     prog, pp = bench.ref_params(wl, g)
-    orc = Oracle.run(g, prog, scheme=GG, sigma=bench.SIGMA, theta=wl["theta"], alpha=bench.ALPHA,
-                     max_iterations=max_iterations, seed=wl["seed"], threads=THREADS,
-                     want_flags=True, **pp)
+    kw = dict(scheme=GG, sigma=bench.SIGMA, theta=wl["theta"], alpha=bench.ALPHA,
+              max_iterations=budget, seed=wl["seed"], threads=THREADS)
+    ref = Reference.run(g, prog, **kw, **pp)
+    assert ref.status == 0, ref.msg
+    orc = Oracle.run(g, prog, want_flags=True, device_flags=dev_flags, tol_unit=NEAR_UNIT[prog],
+                     **kw, **pp)
     assert orc.status == 0, orc.msg
+    assert 2 in ref.modes, "the run must include a superstep"
+
+    # masks, in lock-step
+    real = sum(s["real"] for s in orc.lockstep)
+    adopted = sum(s["adopted"] for s in orc.lockstep)
+    near = sum(s["near"] for s in orc.lockstep)
     mism = int(np.count_nonzero(rep.flags != orc.flags))
-    print(f"{wl['prog']}: {g.e} edges, {int(orc.flags.sum())} active, mask mismatches {mism}")
+    print(f"{name} {wl['prog']}: {g.e} edges, {rep.iterations_run} iterations, "
+          f"{int(orc.flags.sum())} active flags; supersteps {orc.lockstep}; "
+          f"near-threshold edges in the band {near}, decided differently {adopted}, "
+          f"real mismatches {real}, final mask mismatches {mism}")
+    assert all(s["compared"] for s in orc.lockstep)
+    assert real == 0
     assert mism == 0
+
+    # records and properties: against the reference itself unless a
+    # near-threshold edge was adopted (then against the lock-step oracle)
+    base = ref if adopted == 0 else orc
+    assert rep.iterations_run == base.iterations_run
+    assert [int(r.mode) for r in rep.per_iteration] == base.modes
+    assert [r.processed_edges for r in rep.per_iteration] == base.processed_edges
+    assert [r.active_vertices for r in rep.per_iteration] == base.active_vertices
+    if adopted == 0:  # the oracle is the reference restated
+        assert orc.processed_edges == ref.processed_edges
+        assert orc.active_vertices == ref.active_vertices
+    d = np.asarray(rep.final_properties)
+    if wl["prog"] in ("sssp", "wcc"):
+        assert np.array_equal(d, base.props)  # u32 distances / labels, exact
+    else:
+        np.testing.assert_allclose(d.reshape(-1), np.asarray(base.props).reshape(-1),
+                                   rtol=RTOL[wl["prog"]], atol=0)
+    return wl, host
 
 
 def test_c2_sssp_full_scale(ggb, need_reference):
-    wl, rep, ref, host = _run_both(ggb, "c2", 12, want_flags=True)
-    _check_records(rep, ref)
-    d = np.asarray(rep.final_properties)
-    assert np.array_equal(d, ref.props)  # u32 distances, exact
-    _check_masks(wl, rep, host, 12)
+    wl, host = _full(ggb, "c2")
     # the device generator equals the CPU generator at full scale
     cpu = Oracle.rmat(wl["scale"], wl["ef"], wl["seed"], threads=THREADS)
     assert np.array_equal(cpu.off, host.in_offsets)
@@ -100,26 +116,12 @@ def test_c2_sssp_full_scale(ggb, need_reference):
 
 
 def test_c3_wcc_full_scale(ggb, need_reference):
-    wl, rep, ref, host = _run_both(ggb, "c3", 8, want_flags=True)
-    _check_records(rep, ref)
-    assert np.array_equal(np.asarray(rep.final_properties), ref.props)
-    _check_masks(wl, rep, host, 8)
+    _full(ggb, "c3")
 
 
 def test_c4_bp_full_scale(ggb, need_reference):
-    _, rep, ref, _ = _run_both(ggb, "c4", 6)
-    _check_records(rep, ref)
-    np.testing.assert_allclose(np.asarray(rep.final_properties).reshape(-1),
-                               np.asarray(ref.props).reshape(-1), rtol=RTOL["bp"], atol=0)
+    _full(ggb, "c4")
 
 
 def test_c5_pagerank_full_scale(ggb, need_reference):
-    # the single-threaded oracle needs ~150 s for the c5 masks: opt-in
-    # (GGB_FULL_MASKS=1; measured round 1: 0 of 1,844,199,744 edges differ)
-    masks = os.environ.get("GGB_FULL_MASKS") == "1"
-    wl, rep, ref, host = _run_both(ggb, "c5", 6, want_flags=masks)
-    _check_records(rep, ref)
-    if masks:
-        _check_masks(wl, rep, host, 6)
-    np.testing.assert_allclose(np.asarray(rep.final_properties), ref.props, rtol=RTOL["pr"],
-                               atol=0)
+    _full(ggb, "c5")

@@ -97,3 +97,78 @@ def test_bad_files_fail_like_read_binary(ggb, need_reference, tmp_path):
         assert str(dev_err.value) == str(ref_err.value), name
     with pytest.raises(RuntimeError, match="cannot open binary graph"):
         ggb.DeviceGraph.load(str(tmp_path / "missing.bin"))
+
+
+def _ranks(ggb, fn, nranks):
+    """fn(rank, exchange handle) on nranks host threads (in-process transport)."""
+    import threading
+    xs = ggb.Exchange.local_group(nranks)
+    out, errs = [None] * nranks, [None] * nranks
+
+    def work(r):
+        try:
+            out[r] = fn(r, xs[r].handle)
+        except BaseException as e:  # noqa: BLE001 - returned to the caller
+            errs[r] = e
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for x in xs:
+        x.close()
+    return out, errs
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+def test_ggcsr2_stored_out_degrees_are_validated(ggb, tmp_path, nranks):
+    """GGCSR2 carries the out-degrees; a file whose stored degrees are not
+    the sources' counts is rejected with Graph::validate's message
+    (graph.cpp:88-93), also when each rank holds only a slice of the
+    sources (the counts are summed over ranks)."""
+    dg = ggb.DeviceGraph.rmat(12, 8, 9)
+    good = str(tmp_path / "good2.bin")
+    dg.save(good)
+    n, e = dg.n, dg.e
+    dg.close()
+    raw = bytearray(open(good, "rb").read())
+    deg0 = 6 + 24 + (n + 1) * 8 + e * 4  # first stored out-degree (unweighted GGCSR2)
+    v = 5
+    d = int.from_bytes(raw[deg0 + 4 * v: deg0 + 4 * v + 4], "little")
+    raw[deg0 + 4 * v: deg0 + 4 * v + 4] = (d + 1).to_bytes(4, "little")
+    bad = str(tmp_path / "bad2.bin")
+    open(bad, "wb").write(bytes(raw))
+
+    def load(path):
+        def fn(r, x):
+            g = ggb.DeviceGraph.load(path, device=0, rank=r, nranks=nranks, exchange=x) \
+                if nranks > 1 else ggb.DeviceGraph.load(path)
+            g.close()
+            return True
+        return _ranks(ggb, fn, nranks)
+    ok, errs = load(good)
+    assert all(ok) and not any(errs)
+    _, errs = load(bad)
+    assert all(errs)
+    for err in errs:
+        assert str(err) == "graph: out_degree inconsistent with edges"
+
+
+def test_create_validates_sources_and_offsets(ggb):
+    """gg_dev_graph_create on a host CSC view: a source >= n (also when the
+    caller supplies out-degrees) and decreasing offsets fail creation with
+    Graph::validate's conditions (graph.cpp:83-92) instead of reading out of
+    bounds on the device."""
+    n = 6
+    off = np.array([0, 2, 3, 3, 5, 6, 7], np.uint64)
+    src = np.array([1, 2, 0, 5, 1, 3, 4], np.uint32)
+    deg = np.bincount(src, minlength=n).astype(np.uint32)
+    ggb.DeviceGraph.upload(ggb.Graph(n, off, src, None, deg)).close()  # valid
+    bad_src = src.copy()
+    bad_src[4] = n + 3
+    with pytest.raises(ValueError, match="edge source out of range"):
+        ggb.DeviceGraph.upload(ggb.Graph(n, off, bad_src, None, deg))
+    bad_off = off.copy()
+    bad_off[2], bad_off[3] = 4, 3  # 2, 4, 3: decreases (offsets[n] still == e)
+    with pytest.raises(ValueError, match="offsets decrease"):
+        ggb.DeviceGraph.upload(ggb.Graph(n, bad_off, src, None, deg))

@@ -269,14 +269,33 @@ def test_dumbbell_recovery(ggb):  # test_engine.cpp:258-286, acceptance 3
     assert gg.per_iteration[2].mode == ggb.IterationMode.superstep
 
 
-def test_thread_and_launch_invariance(ggb):  # test_engine.cpp:161-182 analogue
-    g = Oracle.power_law(2000, 8.0, 2.1, 3)
-    cfg = ggb.EngineConfig("gg", 0.4, 0.2, 3, 30, 5)
-    a = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(), cfg)
-    cfg8 = ggb.EngineConfig("gg", 0.4, 0.2, 3, 30, 5, threads=8)
-    b = ggb.run(to_graph(ggb, g), ggb.pagerank_spec(), cfg8)
-    assert np.array_equal(a.final_properties, b.final_properties)
-    assert [r.processed_edges for r in a.per_iteration] == [r.processed_edges for r in b.per_iteration]
+@pytest.mark.parametrize("prog", ["pr", "wcc", "sssp", "bp"])
+def test_grid_and_thread_invariance(ggb, prog):  # test_engine.cpp:161-182 analogue
+    """The fold structure is a function of global edge positions only, so
+    properties, flags and per-iteration counts are bit-identical whatever
+    the grid (1 CTA, a few, the occupancy-sized default: tasks land on
+    different warps in a different order, and the superstep chain waits on
+    different predecessors) and whatever cfg.threads says."""
+    g = Oracle.power_law(6000, 10.0, 2.1, 3)
+    if prog == "wcc":
+        g = Oracle.symmetrized(g)
+    if prog == "sssp":
+        g = Oracle.random_graph(4000, 50000, 3, True)
+    program = {"pr": ggb.pagerank_spec(), "wcc": ggb.wcc_spec(), "sssp": ggb.sssp_spec(0, True),
+               "bp": ggb.bp_spec(3, 0.7)}[prog]
+    dg = ggb.DeviceGraph.upload(to_graph(ggb, g))
+    cfg = ggb.EngineConfig("gg", 0.4, 0.05, 3, 30, 5)
+    base = ggb.run(dg, program, cfg, want_flags=True)
+    assert any(r.mode == ggb.IterationMode.superstep for r in base.per_iteration)
+    for grid, threads in ((1, 1), (3, 1), (7, 8), (0, 8)):
+        c = ggb.EngineConfig("gg", 0.4, 0.05, 3, 30, 5, threads=threads)
+        r = ggb.run(dg, program, c, want_flags=True, grid_ctas=grid)
+        assert np.array_equal(np.asarray(r.final_properties).view(np.uint8),
+                              np.asarray(base.final_properties).view(np.uint8)), (grid, threads)
+        assert np.array_equal(r.flags, base.flags), (grid, threads)
+        assert [(x.processed_edges, x.active_vertices) for x in r.per_iteration] == \
+            [(x.processed_edges, x.active_vertices) for x in base.per_iteration]
+    dg.close()
 
 
 # --------------------------------------------------------------------------
@@ -363,18 +382,20 @@ def _exact_graph(n, e, seed, weighted=False):
 def test_list_build_tile_boundaries(ggb, n, e):
     g = _exact_graph(n, e, n + e)
     gw = _exact_graph(n, e, n + e + 1, weighted=True)
-    total = 0
-    # theta is not of the form 1/k: duplicate sources make PR influences
-    # exactly 1/k, and on such an exact tie the run-granular re-association
-    # of the PR fold may round to the other side of theta (the allowed
-    # near-threshold deviation; theta = 0.05 flips one edge of 98309 here)
+    total = adopted = 0
+    # theta = 0.05 = 1/20: duplicate sources make PR influences exactly 1/k,
+    # and on such an exact tie the run-granular re-association of the PR
+    # fold may round to the other side of theta -- the allowed near-threshold
+    # deviation, which the lock-step comparison adopts and counts (parity.py)
     for scheme in ("sp", "gg", "sms"):
-        kw = dict(scheme=scheme, sigma=0.5, theta=0.0437, alpha=2, max_iterations=12, seed=e)
-        total += compare(ggb, g, PR, **kw)[2]
-        total += compare(ggb, g, WCC, **kw)[2]
-        total += compare(ggb, gw, SSSP, graded=True, **kw)[2]  # f64 weights
-        total += compare(ggb, gw, SSSP, graded=True,
-                         device_weights=gw.w.astype(np.float32), **kw)[2]  # f32 weights
+        kw = dict(scheme=scheme, sigma=0.5, theta=0.05, alpha=2, max_iterations=12, seed=e)
+        for r in (compare(ggb, g, PR, **kw)[2], compare(ggb, g, WCC, **kw)[2],
+                  compare(ggb, gw, SSSP, graded=True, **kw)[2],  # f64 weights
+                  compare(ggb, gw, SSSP, graded=True,
+                          device_weights=gw.w.astype(np.float32), **kw)[2]):  # f32 weights
+            total += int(r)
+            adopted += r.adopted
+    print(f"n={n} e={e}: near-threshold edges decided differently: {adopted}")
     assert total == 0
 
 
@@ -409,7 +430,7 @@ def test_weight_ignoring_programs_on_weighted_graphs(ggb, scheme):
     on a weighted graph the sparsified list carries sources only."""
     g = Oracle.random_graph(3000, 40000, 5, True)
     u = Oracle.symmetrized(g)
-    kw = dict(scheme=scheme, sigma=0.5, theta=0.0437, alpha=3, max_iterations=20, seed=9)
+    kw = dict(scheme=scheme, sigma=0.5, theta=0.05, alpha=3, max_iterations=20, seed=9)
     total = 0
     for w in (g.w, g.w.astype(np.float32), g.w.astype(np.uint32)):
         total += compare(ggb, g, PR, device_weights=w, **kw)[2]
