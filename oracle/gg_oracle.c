@@ -732,7 +732,7 @@ int og_run_ex(const og_graph* g, int which, const og_params* params,
                     if (superstep) {                               /* :207-211 */
                         int keep = estatus(infl, cfg->theta);
                         if (ls) {
-                            const int near = fabs(infl - cfg->theta) <=
+                            const int near = ls->tol_unit > 0.0 && fabs(infl - cfg->theta) <=
                                              near_band(ls, e - g->off[v], infl, cfg->theta);
                             n_near += near;
                             if (dev) {

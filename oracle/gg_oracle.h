@@ -117,7 +117,8 @@ int og_run(const og_graph* g, int prog, const og_params* params,
  * safety factor): it bounds how far a re-associated prefix accumulator (the
  * device joins 16-edge runs, engine.hpp:198-211 folds left to right) can
  * move the influence; 0 for the min programs (SSSP, WCC), whose folds are
- * exact under any grouping. */
+ * exact under any grouping (no edge is near-threshold then: an exact tie
+ * with theta is decided identically on both sides). */
 typedef struct og_lockstep {
     const uint32_t* const* dev_bitmaps; /* [n_dev]: device flags right after superstep s (bit e of word e/32), NULL = none */
     uint64_t n_dev;
