@@ -14,18 +14,38 @@ built on the device — the paper's datasets are not used):
   c5 PR   s26 EF28 seed 5 (default: the largest graph; multi-GPU scaling)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5]
+      N > 1 without torchrun: re-launches itself under torch.distributed.run
+      (one process per GPU, NCCL transport); under torchrun WORLD_SIZE must
+      equal N.
+  python bench.py --gpus N --transport local
+      N ranks as host threads sharing ONE GPU (in-process transport): runs
+      the partitioned engine end to end (exchange bytes and time per
+      iteration are reported); not a scaling measurement (n_gpus = 1).
   python bench.py --impl reference ...   (reference CPU engine, rank 0 only)
+
+Beside the device number the line carries: accuracy of the gg run against
+the accurate run (the reference sweep's score, bench.cpp:181-190) and its
+edge ratio; the roofline of the dominant kernel; the end-to-end figure
+through the public API with host buffers; the reference CPU engine on a
+bounded sample (cpu_baseline, rank 0 at N = 1).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
+
+# Both CPU legs (cpu_baseline and --impl reference) run the reference's
+# OpenMP loops under the same settings; set before any OpenMP runtime loads.
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+os.environ.setdefault("OMP_PROC_BIND", "close")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -40,6 +60,9 @@ WORKLOADS = {
 }
 SIGMA, ALPHA = 0.5, 4
 DTYPE = {"pr": "f64", "sssp": "u32", "wcc": "u32", "bp": "f32 storage / f64 arithmetic"}
+# bench.cpp:280-287 default metric per algorithm: 0 top-k, 1 relative, 2 stretch
+METRIC_KIND = {"pr": 0, "bp": 0, "wcc": 1, "sssp": 2}
+METRIC_NAME = {0: "topk", 1: "relative", 2: "stretch"}
 
 
 def log(*a):
@@ -53,13 +76,28 @@ def dist_env():
     return world, rank, local
 
 
-def config_json(args, wl, world):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def omp_env():
+    return {k: os.environ.get(k) for k in ("OMP_WAIT_POLICY", "OMP_PROC_BIND")}
+
+
+def config_json(args, wl, world, transport="nccl"):
+    par = f"dst-partition x{world}" + (f" ({transport})" if world > 1 else "")
     return {
         "workload": f"{args.workload}: {wl['prog'].upper()} on R-MAT s{wl['scale']} EF{wl['ef']} "
                     f"seed {wl['seed']}" + (" symmetrised" if wl["sym"] else ""),
         "scale": wl["scale"], "edge_factor": wl["ef"], "seed": wl["seed"],
         "scheme": "gg", "sigma": SIGMA, "theta": wl["theta"], "alpha": ALPHA,
-        "rmat_abcd": [0.57, 0.19, 0.19, 0.05], "parallelism": f"dst-partition x{world}",
+        "rmat_abcd": [0.57, 0.19, 0.19, 0.05], "parallelism": par,
         "l2": "inputs larger than L2 (CSC >> 126 MB)" if wl["scale"] >= 22
               else "L2-resident graph (no flush: launch-bound parity config)",
     }
@@ -151,6 +189,10 @@ def prop_bytes(wl):
     return {"pr": 8, "sssp": 8, "wcc": 4, "bp": 16}[wl["prog"]]
 
 
+def msg_bytes(wl):  # per-vertex message the exchange carries
+    return {"pr": 8, "sssp": 4, "wcc": 4, "bp": 8}[wl["prog"]]
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -169,6 +211,77 @@ def load_traffic(workload):
         return None, None
 
 
+def device_accuracy(ggb, wl, n, acc_proj, dg, rep, acc_edges):
+    """Score of the gg run against the accurate run on the device (the
+    reference sweep's metric per algorithm, bench.cpp:181-190 / :280-287);
+    both projections stay in HBM."""
+    kind = METRIC_KIND[wl["prog"]]
+    proj = dg.last_projection()
+    if kind == 0:
+        r = ggb.topk_error(proj, acc_proj, max(1, n // 100))
+    elif kind == 1:
+        r = ggb.relative_error(proj, acc_proj)
+    else:
+        r = ggb.stretch_error(proj, acc_proj)
+    return {"metric": METRIC_NAME[kind], "accuracy": round(r.accuracy, 6),
+            "k": max(1, n // 100) if kind == 0 else None,
+            "edge_ratio": round(rep.total_processed_edges / acc_edges, 6) if acc_edges else 1.0}
+
+
+def summarize(args, wl, reps, info, e, per_rank_frac, peak_info):
+    per = [it for r in reps for it in r.per_iteration]
+    approx = [it for it in per if it.mode.name == "approximate"]
+    full = [it for it in per if it.mode.name != "approximate"]
+
+    def gteps(its):  # gather step (edge + vertex kernels) of this rank
+        t = sum(i.kernel_ms for i in its)
+        return (sum(i.processed_edges for i in its) * per_rank_frac / (t / 1e3) / 1e9) if t else None
+
+    def gbs(its, b="edge_bytes", m="edge_ms"):  # algorithmic bytes / CUDA-event time
+        t = sum(getattr(i, m) for i in its)
+        return (sum(getattr(i, b) for i in its) / (t / 1e3) / 1e9) if t else None
+
+    peak, peak_src = peak_info
+    dom = approx if approx else full  # the dominant kernel: the approximate edge gather
+    achieved = gbs(dom)
+    traffic, ncu = load_traffic(args.workload)
+    roofline = {
+        "bound": "hbm", "kernel": "edge_kernel<kEdgePlain> (approximate gather, sparsified CSC)"
+        if approx else "edge_kernel (full gather)",
+        "achieved": round(achieved, 1) if achieved else None, "peak": peak, "peak_source": peak_src,
+        "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
+        "traffic": traffic,
+        "traffic_source": (f"profiles/ncu_{args.workload}.json: ncu --set full, dram read+write of one "
+                           f"launch with {ncu['dominant_kernel_algo_bytes_per_launch']} algorithmic bytes"
+                           if ncu else None),
+        "algo_bytes_per_launch": int(sum(i.edge_bytes for i in dom) / max(len(dom), 1)),
+        "bytes_model": "E_p * (4 src + sizeof(message) + sizeof(weight)); SURVEY §8(d) b_e",
+        "kernel_ms_per_launch": round(sum(i.edge_ms for i in dom) / max(len(dom), 1), 4),
+        "launches": len(dom),
+        "vertex_kernel_gbs": round(gbs(per, "vertex_bytes", "vertex_ms"), 1)
+        if gbs(per, "vertex_bytes", "vertex_ms") else None,
+        "full_gather_edge_gbs": round(gbs(full), 1) if gbs(full) else None,
+    }
+    return roofline, gteps(approx), gteps(full), per
+
+
+def exchange_stats(ggb, wl, world, per, host_out_degree, bounds):
+    """NVLink bytes each rank receives per iteration (the gathered message
+    slots of the other ranks' ranges) and the measured
+    exchange time per iteration (CUDA events around it, this rank)."""
+    import numpy as np
+    if world <= 1:
+        return None
+    od = host_out_degree
+    gathered = [int(np.count_nonzero(od[int(bounds[r]):int(bounds[r + 1])])) for r in range(world)]
+    total = sum(gathered)
+    recv = [(total - gathered[r]) * msg_bytes(wl) for r in range(world)]
+    ex = [it.exchange_ms for it in per if it.exchange_ms]
+    return {"bytes_received_per_iter_per_rank": recv, "max_bytes_received_per_iter": max(recv),
+            "exchange_ms_per_iter_rank0": round(sum(ex) / len(ex), 4) if ex else None,
+            "what": "message slots with out-degree > 0 of the other ranks' ranges, AllGatherV"}
+
+
 def ours(args):
     import numpy as np
     import torch
@@ -176,6 +289,8 @@ def ours(args):
     import paper_2104_10039_b200 as ggb
 
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     torch.cuda.set_device(local)
     dist = None
     exchange = None
@@ -195,6 +310,7 @@ def ours(args):
     program = make_program(ggb, wl, dg, n)
     acc = ggb.run(dg, program, ggb.EngineConfig("accurate", max_iterations=budget_for(wl, n)),
                   device_output=True)
+    acc_proj = ggb.DeviceBuffer.copy(dg.last_projection())
     budget = acc.iterations_run
     cfg = ggb.EngineConfig("gg", SIGMA, wl["theta"], ALPHA, budget, wl["seed"])
     log(f"[rank {rank}] graph n={n} e={e} local={info} accurate iterations={budget} "
@@ -226,50 +342,22 @@ def ours(args):
     value = edges / (ms / 1e3) / 1e9
     launches = sum(r.kernel_launches for r in reps)
 
-    # per-mode GTEPS and the dominant kernel's roofline (CUDA events on the
-    # engine's own stream, recorded around every gather launch)
-    per = [it for r in reps for it in r.per_iteration]
-    approx = [it for it in per if it.mode == ggb.IterationMode.approximate]
-    full = [it for it in per if it.mode != ggb.IterationMode.approximate]
-    frac_rank = info["e_local"] / max(e, 1)
-
-    def gteps(its):  # gather step (edge + vertex kernels) of this rank
-        t = sum(i.kernel_ms for i in its)
-        return (sum(i.processed_edges for i in its) * frac_rank / (t / 1e3) / 1e9) if t else None
-
-    def gbs(its, b="edge_bytes", m="edge_ms"):  # algorithmic bytes / CUDA-event time
-        t = sum(getattr(i, m) for i in its)
-        return (sum(getattr(i, b) for i in its) / (t / 1e3) / 1e9) if t else None
+    # accuracy of the (last) gg run against the accurate run, on the device
+    accuracy = device_accuracy(ggb, wl, n, acc_proj, dg, reps[-1], acc.total_processed_edges)
+    acc_proj.close()
 
     peaks = load_peaks()
-    peak = peaks.get("hbm_gbs", 6650.0)
-    dom = approx if approx else full  # the dominant kernel: the approximate edge gather
-    achieved = gbs(dom)
-    traffic, ncu = load_traffic(args.workload)
-    roofline = {
-        "bound": "hbm", "kernel": "edge_kernel<kEdgePlain> (approximate gather, sparsified CSC)"
-        if approx else "edge_kernel (full gather)",
-        "achieved": round(achieved, 1) if achieved else None, "peak": peak,
-        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if "hbm_gbs" in peaks
-        else "fallback 6650 GB/s (B200_PROFILING.md)",
-        "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
-        "traffic": traffic,
-        "traffic_source": (f"profiles/ncu_{args.workload}.json: ncu --set full, dram read+write of one "
-                           f"launch with {ncu['dominant_kernel_algo_bytes_per_launch']} algorithmic bytes"
-                           if ncu else None),
-        "algo_bytes_per_launch": int(sum(i.edge_bytes for i in dom) / max(len(dom), 1)),
-        "bytes_model": "E_p * (4 src + sizeof(message) + sizeof(weight)); SURVEY §8(d) b_e",
-        "kernel_ms_per_launch": round(sum(i.edge_ms for i in dom) / max(len(dom), 1), 4),
-        "launches": len(dom),
-        "vertex_kernel_gbs": round(gbs(per, "vertex_bytes", "vertex_ms"), 1)
-        if gbs(per, "vertex_bytes", "vertex_ms") else None,
-        "full_gather_edge_gbs": round(gbs(full), 1) if gbs(full) else None,
-    }
+    peak_info = (peaks.get("hbm_gbs", 6650.0),
+                 "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)" if "hbm_gbs" in peaks
+                 else "fallback 6650 GB/s (B200_PROFILING.md)")
+    roofline, g_sp, g_full, per = summarize(args, wl, reps, info, e, info["e_local"] / max(e, 1),
+                                            peak_info)
 
     # ---- end to end through the public API: pinned host CSC -> H2D upload
     # (gg_dev_graph_create), run, D2H of the final properties, every step.
     e2e = None
-    if not args.no_e2e:
+    host = None
+    if not args.no_e2e or world > 1:
         def pinned(count, dt):
             t = torch.empty(int(count) * np.dtype(dt).itemsize, dtype=torch.uint8,
                             pin_memory=True)
@@ -281,6 +369,7 @@ def ours(args):
                                           weights=wl["weights"], device=local)
             host = full_g.to_host(alloc=pinned)
             full_g.close()
+    if not args.no_e2e:
         wsz = host.weights.dtype.itemsize if host.weights is not None else 0
         h2d = (info["v_end"] - info["v_begin"] + 1) * 8 + info["e_local"] * (4 + wsz) + n * 4
         d2h = n * prop_bytes(wl)
@@ -321,15 +410,18 @@ def ours(args):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": round(ems / args.steps, 3),
                "path": "gg_dev_graph_create (pinned host CSC) + gg_run_* + D2H properties"}
-    else:
-        host = None
+
+    xstats = None
+    if world > 1:
+        xstats = exchange_stats(ggb, wl, world, per, host.out_degree,
+                                ggb.partition_plan(host, world))
 
     # ---- reference CPU path beside it (rank 0, N=1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if host is None:
             host = dg.to_host()
-        cpu = reference_sample(wl, host, n, program_seed=wl["seed"], repeats=1)
+        cpu = cpu_baseline_sample(wl, host)
 
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world,
@@ -340,11 +432,14 @@ def ours(args):
                                                  "max_iterations": budget,
                                                  "iterations_per_step": reps[0].iterations_run,
                                                  "edges_per_step": reps[0].total_processed_edges},
-        "gteps_sparsified_kernel": round(gteps(approx), 3) if gteps(approx) else None,
-        "gteps_full_kernel": round(gteps(full), 3) if gteps(full) else None,
+        "gteps_sparsified_kernel": round(g_sp, 3) if g_sp else None,
+        "gteps_full_kernel": round(g_full, 3) if g_full else None,
+        "accuracy": accuracy,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk,
     }
+    if xstats:
+        out["exchange"] = xstats
     if rank == 0:
         print(json.dumps(out), flush=True)
     if exchange:
@@ -354,8 +449,94 @@ def ours(args):
         dist.destroy_process_group()
 
 
+def ours_local(args):
+    """N ranks as host threads on one GPU through the in-process transport
+    (gg_exchange_local_group): the whole partitioned engine path, exchange
+    included, on one device. Graph slices are created one rank at a time
+    (bounded peak memory); the timed runs of all ranks overlap."""
+    import torch
+
+    import paper_2104_10039_b200 as ggb
+
+    N = args.gpus
+    wl = WORKLOADS[args.workload]
+    torch.cuda.set_device(0)
+    xs = ggb.Exchange.local_group(N)
+    create_lock = threading.Lock()
+    res = [None] * N
+    errs = []
+    start = threading.Barrier(N)
+
+    def work(r):
+        try:
+            with create_lock:
+                dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],
+                                          weights=wl["weights"], device=0, rank=r, nranks=N,
+                                          exchange=xs[r].handle)
+            program = make_program(ggb, wl, dg, dg.n)
+            acc = ggb.run(dg, program, ggb.EngineConfig("accurate",
+                                                       max_iterations=budget_for(wl, dg.n)),
+                          device_output=True)
+            cfg = ggb.EngineConfig("gg", SIGMA, wl["theta"], ALPHA, acc.iterations_run, wl["seed"])
+            for _ in range(args.warmup):
+                ggb.run(dg, program, cfg, device_output=True)
+            start.wait()
+            t0 = time.perf_counter()
+            reps = [ggb.run(dg, program, cfg, timing=True, device_output=True)
+                    for _ in range(args.steps)]
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            res[r] = dict(info=dg.info(), reps=reps, wall=wall, budget=acc.iterations_run,
+                          n=dg.n, e=dg.e, od=dg.out_degree() if r == 0 else None)
+            dg.close()
+        except BaseException as ex:  # noqa: BLE001
+            errs.append(ex)
+            try:
+                start.abort()
+            except Exception:
+                pass
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(N)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for x in xs:
+        x.close()
+    if errs:
+        raise errs[0]
+    n, e = res[0]["n"], res[0]["e"]
+    wall = max(r["wall"] for r in res)
+    edges = sum(rep.total_processed_edges for rep in res[0]["reps"])  # every rank reports the total
+    per = [it for rep in res[0]["reps"] for it in rep.per_iteration]
+    import numpy as np
+    bounds = [0]
+    for r in res:
+        bounds.append(r["info"]["v_end"])
+    xstats = exchange_stats(ggb, wl, N, per, res[0]["od"], np.array(bounds, np.uint64))
+    xstats["exchange_ms_per_iter_per_rank"] = [
+        round(sum(it.exchange_ms for rep in r["reps"] for it in rep.per_iteration) /
+              max(1, sum(len(rep.per_iteration) for rep in r["reps"])), 4) for r in res]
+    out = {
+        "metric": METRIC, "value": round(edges / wall / 1e9, 4), "unit": "GTEPS", "n_gpus": 1,
+        "ranks": N, "transport": "local: ranks are host threads sharing one GPU (host barriers + "
+                                 "device copies); not a scaling measurement",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": DTYPE[wl["prog"]], "data": "synthetic R-MAT (seeded, built on device)",
+        "config": config_json(args, wl, N, "local") | {
+            "vertices": n, "edges": e, "max_iterations": res[0]["budget"],
+            "iterations_per_step": res[0]["reps"][0].iterations_run,
+            "edges_per_rank": [r["info"]["e_local"] for r in res],
+            "vertex_ranges": [[r["info"]["v_begin"], r["info"]["v_end"]] for r in res]},
+        "exchange": xstats,
+        "timing": "host wall clock around the ranks' runs (threads share one device)",
+        "gpu_launches": sum(rep.kernel_launches for r in res for rep in r["reps"]),
+    }
+    print(json.dumps(out), flush=True)
+
+
 # --------------------------------------------------------------------------
-# reference arm (the unmodified reference, oracle/_ref/libggref.so)
+# reference CPU engine (the unmodified reference, oracle/_ref/libggref.so)
 # --------------------------------------------------------------------------
 def ref_inputs(wl, host_graph=None):
     """Host CSC for the reference: from our arm's export, else the CPU
@@ -390,65 +571,147 @@ def ref_params(wl, g):
     return BP_EDGE, dict(prior_table=Oracle.bp_priors(g.n, wl["seed"]), epsilon=1e-6)
 
 
-SAMPLE_ITERS = 1
+STEP_ITERS = 1            # --impl reference: each step = the first (approximate) iteration
+WINDOW_ITERS = ALPHA + 1  # cpu_baseline: one window of alpha approximate iterations + a superstep
 
 
-def reference_sample(wl, host_graph, n, program_seed, repeats=1, handle=None, g=None):
-    """Bounded sample: the reference gg::run (gg scheme, all host threads)
-    capped at SAMPLE_ITERS iteration(s); GTEPS from its own RunReport."""
+def _mode_gteps(r, mode):
+    e = sum(pe for m, pe in zip(r.modes, r.processed_edges) if m == mode)
+    w = sum(ws for m, ws in zip(r.modes, r.wall_seconds) if m == mode)
+    return (round(e / w / 1e9, 5) if w else None), e, w
+
+
+def reference_window(wl, g, handle=None, threads=None, iters=WINDOW_ITERS):
+    """The reference gg::run on the workload capped at `iters` iterations
+    (default: alpha approximate iterations + one superstep); per-mode GTEPS
+    from its own RunReport (processed_edges / wall_seconds per iteration)."""
     from oracle.oracle import GG, Reference
+    prog, pp = ref_params(wl, g)
+    cores = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = Reference.run(g, prog, scheme=GG, sigma=SIGMA, theta=wl["theta"], alpha=ALPHA,
+                      max_iterations=iters, seed=wl["seed"], threads=cores, handle=handle, **pp)
+    elapsed = time.perf_counter() - t0
+    assert r.status == 0, r.msg
+    sp, esp, wsp = _mode_gteps(r, 0)
+    full, efu, wfu = _mode_gteps(r, 2)
+    wall = sum(r.wall_seconds)
+    return {"value": round(r.total_processed_edges / wall / 1e9, 5) if wall else None,
+            "sparsified": sp, "full": full, "iterations": r.iterations_run,
+            "edges": r.total_processed_edges, "elapsed_s": round(elapsed, 2), "cores": cores}
+
+
+def reference_one_thread(wl, g, frac=16):
+    """1-thread reference rate on a bounded sample: the destination prefix
+    holding ~E/frac in-edges (all sources still range over every vertex, so
+    the gathers touch the whole property array), first iteration."""
+    from oracle.oracle import CSC
+    import numpy as np
+    k = int(np.searchsorted(g.off, g.off[-1] // frac))
+    sub = CSC(g.n, np.concatenate([g.off[:k + 1], np.full(g.n - k, g.off[k], np.uint64)]),
+              g.src[:int(g.off[k])], None if g.w is None else g.w[:int(g.off[k])])
+    r = reference_window(wl, sub, threads=1, iters=1)
+    r["sample"] = (f"destinations [0, {k}) ({int(g.off[k])} in-edges, 1/{frac} of E; sources over all "
+                   f"{g.n} vertices), first iteration, 1 thread")
+    return r
+
+
+def cpu_baseline_sample(wl, host_graph):
+    """cpu_baseline of our arm: the reference engine on the same graph,
+    all host threads, one window of alpha approximate iterations plus one
+    superstep (~30 s at c5)."""
+    from oracle.oracle import Reference
     if not Reference.available():
         return None
-    g = g if g is not None else ref_inputs(wl, host_graph)
-    prog, pp = ref_params(wl, g)
-    own = handle is None
-    h = handle if handle is not None else Reference.graph(g)
-    cores = os.cpu_count() or 1
-    edges = wall = 0
-    t0 = time.perf_counter()
-    for _ in range(repeats):
-        r = Reference.run(g, prog, scheme=GG, sigma=SIGMA, theta=wl["theta"], alpha=ALPHA,
-                          max_iterations=SAMPLE_ITERS, seed=program_seed, threads=cores,
-                          handle=h, **pp)
-        edges += r.total_processed_edges
-        wall += sum(r.wall_seconds)
-    elapsed = time.perf_counter() - t0
-    if own:
-        Reference.free(h)
-    return {"value": round(edges / wall / 1e9, 5) if wall else None, "unit": "GTEPS",
-            "cores": cores, "kind": "reference",
+    g = ref_inputs(wl, host_graph)
+    w = reference_window(wl, g)
+    cores = w["cores"]
+    return {"value": w["value"], "unit": "GTEPS", "cores": cores, "kind": "reference",
+            "sparsified": w["sparsified"], "full": w["full"],
+            "cpu_model": cpu_model(), "omp": omp_env(),
             "sample": f"reference gg::run (oracle/_ref, OMP threads={cores}) on the same graph, "
-                      f"max_iterations={SAMPLE_ITERS} (first approximate iteration), x{repeats}; "
-                      f"GTEPS = processed_edges / RunReport wall_seconds; "
-                      f"{elapsed:.1f}s incl. serial sparsify/setup"}
+                      f"max_iterations={WINDOW_ITERS} ({ALPHA} approximate iterations + 1 superstep, "
+                      f"gg scheme); GTEPS = processed_edges / RunReport wall_seconds (sparsify "
+                      f"outside); {w['elapsed_s']} s of CPU run incl. serial sparsify"}
+
+
+def reference_accuracy(wl, g, handle):
+    """The reference's own score of its gg run against its accurate run
+    (bench.cpp:133-190 protocol: accurate run to convergence within the
+    default budget, gg run capped at its iterations)."""
+    import numpy as np
+
+    from oracle.oracle import ACCURATE, GG, WCC, BP_EDGE, Reference
+    prog, pp = ref_params(wl, g)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    a = Reference.run(g, prog, scheme=ACCURATE, max_iterations=budget_for(wl, g.n), seed=wl["seed"],
+                      threads=cores, handle=handle, **pp)
+    r = Reference.run(g, prog, scheme=GG, sigma=SIGMA, theta=wl["theta"], alpha=ALPHA,
+                      max_iterations=a.iterations_run, seed=wl["seed"], threads=cores, handle=handle,
+                      **pp)
+
+    def proj(x):
+        x = np.asarray(x)
+        if prog == BP_EDGE:
+            return x[:, 0].astype(np.float64)
+        if prog == WCC:
+            return x.astype(np.float64)
+        return x.astype(np.float64)
+    kind = METRIC_KIND[wl["prog"]]
+    k = max(1, g.n // 100)
+    err = Reference.metric(kind, proj(r.props), proj(a.props), k)
+    return {"metric": METRIC_NAME[kind], "accuracy": round((1.0 - err) * 100.0, 6),
+            "k": k if kind == 0 else None,
+            "edge_ratio": round(r.total_processed_edges / a.total_processed_edges, 6)
+            if a.total_processed_edges else 1.0,
+            "accurate_iterations": a.iterations_run, "gg_iterations": r.iterations_run,
+            "elapsed_s": round(time.perf_counter() - t0, 1)}
 
 
 def reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle.oracle import Reference
+    from oracle.oracle import GG, Reference
     wl = WORKLOADS[args.workload]
     if not Reference.available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libggref.so not built (needs /root/reference)"}))
         return
-    os.environ.setdefault("OMP_WAIT_POLICY", "passive")
     t = time.perf_counter()
     g = ref_inputs(wl)
     h = Reference.graph(g)
     log(f"reference inputs n={g.n} e={g.e} in {time.perf_counter() - t:.1f}s")
+    prog, pp = ref_params(wl, g)
+    cores = os.cpu_count() or 1
+
+    def step():
+        r = Reference.run(g, prog, scheme=GG, sigma=SIGMA, theta=wl["theta"], alpha=ALPHA,
+                          max_iterations=STEP_ITERS, seed=wl["seed"], threads=cores, handle=h, **pp)
+        assert r.status == 0, r.msg
+        return r
     for _ in range(args.warmup):
-        reference_sample(wl, None, g.n, wl["seed"], handle=h, g=g)
+        step()
     t0 = time.perf_counter()
-    samples = [reference_sample(wl, None, g.n, wl["seed"], handle=h, g=g)
-               for _ in range(args.steps)]
+    samples = [step() for _ in range(args.steps)]
     elapsed = time.perf_counter() - t0
+    edges = sum(r.total_processed_edges for r in samples)
+    wall = sum(sum(r.wall_seconds) for r in samples)
+    value = round(edges / wall / 1e9, 6) if wall else None
+    # beyond the timed steps: per-mode rates over a window with a superstep,
+    # the 1-thread rate, and the reference's own accuracy
+    window = reference_window(wl, g, handle=h)
+    one = reference_one_thread(wl, g)
+    acc = reference_accuracy(wl, g, h) if not args.no_accuracy else None
     Reference.free(h)
-    vals = [s["value"] for s in samples if s and s["value"]]
-    value = statistics.mean(vals) if vals else None
-    cpu = dict(samples[0])
-    cpu["value"] = value
+    cpu = {"value": value, "unit": "GTEPS", "cores": cores, "kind": "reference",
+           "sparsified": window["sparsified"], "full": window["full"],
+           "window": window, "one_thread": one, "cpu_model": cpu_model(), "omp": omp_env(),
+           "sample": f"reference gg::run (oracle/_ref, OMP threads={cores}), gg scheme, each step "
+                     f"max_iterations={STEP_ITERS} (the first approximate iteration); GTEPS = "
+                     f"processed_edges / RunReport wall_seconds (sparsify outside); window = "
+                     f"{WINDOW_ITERS} iterations incl. a superstep, once"}
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -456,10 +719,19 @@ def reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[wl["prog"]],
         "data": "synthetic R-MAT (seeded, CPU generator)",
         "config": config_json(args, wl, world) | {"vertices": g.n, "edges": g.e},
+        "accuracy": acc,
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -469,16 +741,25 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5")
+    ap.add_argument("--transport", choices=["nccl", "local"], default="nccl")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true", help="reference arm: skip its accuracy runs")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rule: W >= 3)")
         args.warmup = 3
     if args.impl == "reference":
-        reference(args)
-    else:
-        ours(args)
+        return reference(args)
+    if args.transport == "local" and args.gpus > 1:
+        return ours_local(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    ours(args)
 
 
 if __name__ == "__main__":
