@@ -200,6 +200,35 @@ void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e, cons
                              g.stream));  // sentinel run_i[nruns] = nz - 1
 }
 
+// Position order of the local vertices (graph.cuh): rows (non-empty, in
+// vertex order) at [0, R), in-degree-0 vertices at [R, nloc).
+__global__ void positions_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
+                                 uint64_t nloc, uint64_t nrows, uint64_t v_begin,
+                                 const uint32_t* __restrict__ slot_of,
+                                 const uint32_t* __restrict__ outdeg, uint32_t* __restrict__ vid_of_p,
+                                 uint32_t* __restrict__ slot_p, uint32_t* __restrict__ deg_p) {
+    for (uint64_t lv = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; lv < nloc;
+         lv += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = flag[lv] ? idx[lv] : nrows + (lv - idx[lv]);
+        vid_of_p[p] = (uint32_t)lv;
+        slot_p[p] = slot_of[v_begin + lv];
+        deg_p[p] = outdeg[v_begin + lv];
+    }
+}
+
+void build_full(DevGraph& g) {
+    build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
+    g.nrows = g.full.nz;
+    g.vid_of_p = static_cast<uint32_t*>(dev_alloc((g.nloc + 1) * 4, g.stream));
+    g.slot_p = static_cast<uint32_t*>(dev_alloc((g.nloc + 1) * 4, g.stream));
+    g.deg_p = static_cast<uint32_t*>(dev_alloc((g.nloc + 1) * 4, g.stream));
+    if (!g.nloc) return;
+    positions_kernel<<<grid_for(g.nloc, 256), 256, 0, g.stream>>>(
+        g.ws.get<uint32_t>("full.nzflag", g.nloc + 1), g.ws.get<uint32_t>("full.nzidx", g.nloc + 1),
+        g.nloc, g.nrows, g.v_begin, g.slot_of, g.outdeg, g.vid_of_p, g.slot_p, g.deg_p);
+    GGB_CUDA(cudaGetLastError());
+}
+
 // --------------------------------------------------------------------------
 // bitmap -> sparsified CSC
 // --------------------------------------------------------------------------
@@ -539,9 +568,10 @@ sp_layout_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
     }
 }
 
-// Layout of the sparsified list (kept edges at `pad`): s_off, nz_*, run map.
-// Asynchronous (the non-empty count stays on the device: the edge kernel
-// reads the run_i[nruns] sentinel instead).
+// Layout of the sparsified list (kept edges at `pad`) in ROW space: s_off[p]
+// for the rows p in [0, R] (the in-degree-0 vertices keep nothing), nz_vid =
+// the rows with kept edges, run map. Asynchronous (the non-empty count stays
+// on the device: the edge kernel reads the run_i[nruns] sentinel instead).
 static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint64_t* wpref,
                                 uint64_t* s_off, uint64_t pad, uint64_t kept, ListMeta& meta) {
     meta.pad = pad;
@@ -549,19 +579,19 @@ static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint6
     meta.ntasks = kept ? (pad + kept + kChunkEdges - 1) / kChunkEdges : 0;
     meta.nruns = meta.ntasks * kWarp;
     meta.nz = 0;  // on the device only
-    meta.nz_vid = g.ws.get<uint32_t>("sp.nz_vid", g.nloc + 1);
-    meta.nz_start = g.ws.get<uint64_t>("sp.nz_start", g.nloc + 1);
+    meta.nz_vid = g.ws.get<uint32_t>("sp.nz_vid", g.nrows + 1);
+    meta.nz_start = g.ws.get<uint64_t>("sp.nz_start", g.nrows + 1);
     uint32_t* marks = g.ws.get<uint32_t>("sp.runmark", meta.nruns + 1);
     meta.run_i = g.ws.get<uint32_t>("sp.run_i", meta.nruns + 1);
     if (meta.nruns) GGB_CUDA(cudaMemsetAsync(marks, 0, meta.nruns * 4, g.stream));
-    const uint64_t ntiles = (g.nloc + 1 + kLayoutTile - 1) / kLayoutTile;
+    const uint64_t ntiles = (g.nrows + 1 + kLayoutTile - 1) / kLayoutTile;
     auto* tstate = g.ws.get<unsigned long long>("sp.tstate", ntiles + 1);
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
     GGB_CUDA(cudaMemsetAsync(tstate, 0, (ntiles + 1) * 8, g.stream));
     static const int per_sm = occupancy_grid((const void*)sp_layout_kernel, 256, 0, 1);
     const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)per_sm * g.num_sms);
-    sp_layout_kernel<<<gr, 256, 0, g.stream>>>(g.off, g.nloc, bitmap, wpref, pad, meta.nruns, s_off,
-                                               meta.nz_vid, meta.nz_start, marks, meta.run_i,
+    sp_layout_kernel<<<gr, 256, 0, g.stream>>>(g.full.nz_start, g.nrows, bitmap, wpref, pad, meta.nruns,
+                                               s_off, meta.nz_vid, meta.nz_start, marks, meta.run_i,
                                                tstate, ticket, ntiles);
     GGB_CUDA(cudaGetLastError());
     if (!meta.nruns) return;
@@ -810,22 +840,25 @@ void export_sources(const DevGraph& g, uint32_t* host_out) {
     dev_free(tmp, g.stream);
 }
 
-__global__ void superstep_invalid_kernel(uint32_t nloc, uint32_t v_begin,
-                                         const uint8_t* __restrict__ st_cur,
-                                         const uint8_t* __restrict__ st_next,
+// Rows only: an in-degree-0 vertex keeps no edges, so its condition is its
+// pre-iteration status alone and the vertex kernel reports it directly.
+__global__ void superstep_invalid_kernel(uint32_t nrows, uint32_t v_begin,
+                                         const uint32_t* __restrict__ vid_of_p,
+                                         const uint8_t* __restrict__ st,
                                          const uint64_t* __restrict__ s_off,
                                          IterCounters* __restrict__ ctr) {
     if (!__ldg(&ctr->any_invalid)) return;  // the common case: nothing to rescan
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nloc; v += gridDim.x * blockDim.x) {
-        if ((st_next[v] & kStInvalid) && ((st_cur[v] & kStActive) || s_off[v + 1] > s_off[v]))
-            atomicMin(&ctr->bad_min, v_begin + v);
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nrows; p += gridDim.x * blockDim.x) {
+        const uint8_t s = st[p];
+        if ((s & kStInvalid) && ((s & kStWasActive) || s_off[p + 1] > s_off[p]))
+            atomicMin(&ctr->bad_min, v_begin + vid_of_p[p]);
     }
 }
 
-void launch_superstep_invalid(DevGraph& g, const uint8_t* st_cur, const uint8_t* st_next,
-                              const uint64_t* s_off, void* ctr) {
-    superstep_invalid_kernel<<<grid_for(g.nloc, 256), 256, 0, g.stream>>>(
-        (uint32_t)g.nloc, (uint32_t)g.v_begin, st_cur, st_next, s_off,
+void launch_superstep_invalid(DevGraph& g, const uint8_t* st, const uint64_t* s_off, void* ctr) {
+    if (!g.nrows) return;
+    superstep_invalid_kernel<<<grid_for(g.nrows, 256), 256, 0, g.stream>>>(
+        (uint32_t)g.nrows, (uint32_t)g.v_begin, g.vid_of_p, st, s_off,
         static_cast<IterCounters*>(ctr));
     GGB_CUDA(cudaGetLastError());
 }
@@ -842,17 +875,23 @@ DevGraph::~DevGraph() {
     dev_free(outdeg, stream);
     dev_free(slot_of, stream);
     dev_free(vtx_of_slot, stream);
+    dev_free(vid_of_p, stream);
+    dev_free(slot_p, stream);
+    dev_free(deg_p, stream);
     if (stream) {
         cudaStreamSynchronize(stream);
         cudaStreamDestroy(stream);
     }
 }
 
+// slot 0 stands for "iteration 0": every status starts active, so the
+// first vertex kernel walks the in-degree-0 positions too
 __global__ void reset_counters_kernel(IterCounters* __restrict__ c, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
         IterCounters z{};
         z.bad_min = 0xffffffffu;
+        z.empty_active = i == 0 ? 1u : 0u;
         c[i] = z;
     }
 }

@@ -223,7 +223,7 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
                 GGB_CUDA(cudaGetLastError());
             }
             check_offsets(g, bad + 1);
-            build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
+            build_full(g);
             for (size_t k = 0; k < up.chunk.size(); ++k) {
                 const uint64_t b = std::min(g.e_loc, k * step), e = std::min(g.e_loc, b + step);
                 GGB_CUDA(cudaStreamWaitEvent(g.stream, up.chunk[k], 0));
@@ -311,7 +311,7 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
                 if (r.w) dev_free(r.w, g.stream);
             }
             assign_slots(g);
-            build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
+            build_full(g);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
             delete h;

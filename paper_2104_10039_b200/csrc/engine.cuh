@@ -50,10 +50,13 @@ struct RunIO {
     int out_states = 1;
 };
 
+// Initial messages of every (global) vertex, and the owned vertices'
+// properties and statuses by position (engine.hpp:163-167).
 template <class P>
 __global__ void init_kernel(P prog, uint64_t n, uint32_t v_begin, uint32_t nloc,
                             const uint32_t* __restrict__ outdeg,
                             const uint32_t* __restrict__ slot_of,
+                            const uint32_t* __restrict__ vid_of_p,
                             typename P::Message* __restrict__ msg,
                             typename P::Property* __restrict__ prop, uint8_t* __restrict__ st) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
@@ -62,11 +65,20 @@ __global__ void init_kernel(P prog, uint64_t n, uint32_t v_begin, uint32_t nloc,
         uint32_t deg = 0;
         if constexpr (P::kNeedsDegree) deg = outdeg[v];
         msg[slot_of[v]] = prog.message(p, deg);
-        if (v >= v_begin && v < (uint64_t)v_begin + nloc) {
-            prop[v - v_begin] = p;
-            st[v - v_begin] = kStActive;  // status starts at 1 (engine.hpp:166)
+        if (v < nloc) {  // position v of this rank
+            prop[v] = prog.init_property(v_begin + vid_of_p[v], n);
+            st[v] = kStActive;  // status starts at 1 (engine.hpp:166)
         }
     }
+}
+
+// position order -> vertex order (out[lv] = props[p], lv = vid_of_p[p])
+template <class T>
+__global__ void to_vertex_order_kernel(const T* __restrict__ by_pos, const uint32_t* __restrict__ vid_of_p,
+                                       uint64_t nloc, T* __restrict__ out) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nloc;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        out[vid_of_p[p]] = by_pos[p];
 }
 
 template <class P>
@@ -186,9 +198,13 @@ struct Engine {
         g.project_last = nullptr;  // no valid run until this one completes
         const unsigned cap = io.opts ? io.opts->grid_ctas : 0u;
 
-        Msg* msg[2] = {ws.get<Msg>("msg0", n), ws.get<Msg>("msg1", n)};
+        // one message buffer: an iteration's gathers complete before its
+        // vertex kernel rewrites the messages (same stream); per-vertex state
+        // by position (graph.cuh)
+        Msg* msg = ws.get<Msg>("msg", n);
         Prop* prop = ws.get<Prop>("prop", nloc + 1);
-        uint8_t* st[2] = {ws.get<uint8_t>("st0", nloc + 1), ws.get<uint8_t>("st1", nloc + 1)};
+        uint8_t* st = ws.get<uint8_t>("st", nloc + 1);
+        const uint64_t R = g.nrows;
         // Counters live in a ring of kRing slots: iteration u accumulates into
         // ring[u % kRing] and its vertex kernel resets ring[(u + 1) % kRing]
         // for the next one, so no memset is enqueued per iteration and a
@@ -198,7 +214,7 @@ struct Engine {
             static_cast<IterCounters*>(g.host_counters(kRing * sizeof(IterCounters)));
         reset_counters_kernel<<<1, kRing, 0, g.stream>>>(ring, kRing);
         GGB_CUDA(cudaGetLastError());
-        Acc* acc_out = ws.get<Acc>("acc_out", nloc + 1);
+        Acc* acc_out = ws.get<Acc>("acc_out", R + 1);
         const uint64_t ntask_cap = g.full.ntasks + 2;
         Acc* hv = ws.get<Acc>("hv", ntask_cap);
         Acc* tv = ws.get<Acc>("tv", ntask_cap);
@@ -219,15 +235,14 @@ struct Engine {
         cudaEvent_t e4 = timing ? g.event(4) : nullptr, e5 = timing ? g.event(5) : nullptr;
         cudaEvent_t e6 = timing ? g.event(6) : nullptr, e7 = timing ? g.event(7) : nullptr;
 
-        init_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, n, (uint32_t)g.v_begin,
-                                                         (uint32_t)nloc, g.outdeg, g.slot_of, msg[0],
-                                                         prop, st[0]);
+        init_kernel<P><<<grid1d(std::max<uint64_t>(n, nloc)), 256, 0, g.stream>>>(
+            prog, n, (uint32_t)g.v_begin, (uint32_t)nloc, g.outdeg, g.slot_of, g.vid_of_p, msg, prop, st);
         GGB_CUDA(cudaGetLastError());
         ++launches;
         uint64_t kept = g.e_loc;
         if (sparse) {  // engine.hpp:151-161
             bitmap = ws.get<uint32_t>("bitmap", nwords + 1);
-            s_off = ws.get<uint64_t>("s_off", nloc + 1);
+            s_off = ws.get<uint64_t>("s_off", R + 1);
             s_src = ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
             s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
             if (g.pre_sparse && g.pre_sigma == cfg.sigma && g.pre_seed == cfg.seed) {
@@ -240,7 +255,7 @@ struct Engine {
             }
         }
         g.pre_sparse = false;  // one run uses it (its supersteps rewrite the bitmap)
-        const uint64_t* a_off = sparse ? s_off : g.off;
+        const uint64_t* a_off = sparse ? s_off : g.full.nz_start;  // by row
         // the hottest message slots (lowest ids: hot-first layout) are pinned in
         // L2 with evict_last; with several ranks each range has its own hot
         // prefix and every gather uses evict_normal.
@@ -259,7 +274,6 @@ struct Engine {
         const uint32_t l2_limit =
             g.nranks == 1 ? (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg)) : 0u;
 
-        int cur = 0;
         uint64_t iterations_run = 0, total_edges = 0;
         double total_wall = 0.0;
         // Iterations are enqueued in batches: a stretch of consecutive
@@ -282,7 +296,6 @@ struct Engine {
             auto ev = [&](int k, int i) { return B == 1 ? g.event(i) : g.batch_event(4 * k + i); };
             for (int k = 0; k < B; ++k) {
             const uint64_t u = t + k;
-            const int cu = cur ^ (k & 1);
             const int mode = mode_for(cfg.scheme, u, cfg.alpha);
             const bool approx = mode == GG_MODE_APPROXIMATE;
             super = mode == GG_MODE_SUPERSTEP;
@@ -292,15 +305,15 @@ struct Engine {
             ea.src = approx ? s_src : g.src;
             ea.w = static_cast<const W*>(approx ? s_w : g.w);
             ea.run_i = L.run_i;
-            ea.nz_vid = L.nz_vid;
+            ea.nz_row = approx ? L.nz_vid : nullptr;  // the full list's rows are its nz indices
             ea.nz_start = L.nz_start;
             ea.pad = L.pad;
             ea.e_end = L.e_end();
             ea.ntasks = L.ntasks;
             ea.nruns = L.nruns;
             ea.a_off = a_off;
-            ea.st_cur = st[cu];
-            ea.msg_cur = msg[cu];
+            ea.st_cur = st;
+            ea.msg_cur = msg;
             ea.hot_limit = hot_limit;
             ea.l2_limit = l2_limit;
             ea.cold_last = msgs_fit_l2 ? 1u : 0u;
@@ -320,22 +333,23 @@ struct Engine {
             va.n = n;
             va.v_begin = (uint32_t)g.v_begin;
             va.nloc = (uint32_t)nloc;
-            va.off = approx ? s_off : g.off;
+            va.nrows = (uint32_t)R;
+            va.off = approx ? s_off : g.full.nz_start;
             va.pad = L.pad;
             va.a_off = a_off;
-            va.st_cur = st[cu];
-            va.st_next = st[cu ^ 1];
+            va.st = st;
             va.prop = prop;
-            va.msg_cur = msg[cu];
-            va.msg_next = msg[cu ^ 1];
-            va.outdeg = g.outdeg;
-            va.slot_of = g.slot_of;
+            va.msg = msg;
+            va.vid_of_p = g.vid_of_p;
+            va.slot_p = g.slot_p;
+            va.deg_p = g.deg_p;
             va.acc_out = acc_out;
             va.hv = hv;
             va.tv = tv;
             IterCounters* ctr = ring + u % kRing;
             va.ctr = ctr;
             va.ctr_next = ring + (u + 1) % kRing;
+            va.ctr_prev = ring + (u - 1) % kRing;  // u = 1: slot 0 = "all statuses active"
             va.stop_if = ea.stop_if;
 
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 0), g.stream));
@@ -364,12 +378,12 @@ struct Engine {
                                       timing ? e5 : nullptr, &launches);
                 // bad-vertex rescan against the kept counts; exits at once on
                 // the device unless the vertex kernel saw an invalid property
-                launch_superstep_invalid(g, st[cu], st[cu ^ 1], s_off, ctr);
+                launch_superstep_invalid(g, st, s_off, ctr);
                 ++launches;
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
                 if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
-                exchange_slices(g, msg[cu ^ 1], sizeof(Msg), /*slots=*/true);
+                exchange_slices(g, msg, sizeof(Msg), /*slots=*/true);
                 exchange_counters(g, ctr);
                 if (timing) GGB_CUDA(cudaEventRecord(e7, g.stream));
             }
@@ -422,7 +436,6 @@ struct Engine {
                 iterations_run = u;
                 total_edges += hc.gathered;
                 total_wall += wall;
-                cur ^= 1;                               // engine.hpp:238-239
                 if (!hc.changed) {                      // engine.hpp:240
                     done = true;
                     break;
@@ -431,16 +444,16 @@ struct Engine {
             t += B;
         }
 
-        // final properties (engine.hpp:243)
-        // owned properties (vertex order) gathered from every rank
-        // (one rank: the owned properties are all of them, no copy)
-        Prop* final_all = prop;
-        if (g.nranks > 1) {
-            final_all = ws.get<Prop>("final", n);
-            GGB_CUDA(cudaMemcpyAsync(final_all + g.v_begin, prop, nloc * sizeof(Prop),
-                                     cudaMemcpyDeviceToDevice, g.stream));
-            exchange_slices(g, final_all, sizeof(Prop));
+        // final properties (engine.hpp:243): owned positions back to vertex
+        // order, gathered from every rank
+        Prop* final_all = ws.get<Prop>("final", n);
+        if (nloc) {
+            to_vertex_order_kernel<Prop><<<grid1d(nloc), 256, 0, g.stream>>>(prop, g.vid_of_p, nloc,
+                                                                             final_all + g.v_begin);
+            GGB_CUDA(cudaGetLastError());
+            ++launches;
         }
+        if (g.nranks > 1) exchange_slices(g, final_all, sizeof(Prop));
         g.project_last = [&g, prog, final_all, n]() -> const double* {  // metrics.cu
             double* proj = g.ws.get<double>("proj", n + 1);
             export_kernel<P><<<grid1d(n), 256, 0, g.stream>>>(prog, final_all, n, 1, proj);

@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <condition_variable>
 #include <mutex>
 #include <vector>
@@ -204,6 +205,7 @@ void exchange_counters(DevGraph& g, void* ctr_v) {
             s.processed += c.processed;
             s.changed += c.changed;
             s.any_invalid += c.any_invalid;
+            s.empty_active += c.empty_active;
             s.bad_min = std::min(s.bad_min, c.bad_min);
         }
         L.barrier();
@@ -216,7 +218,10 @@ void exchange_counters(DevGraph& g, void* ctr_v) {
     nccl_check(api.GroupStart(), "ncclGroupStart");
     nccl_check(api.AllReduce(&ctr->gathered, &ctr->gathered, 2, ncclUint64, ncclSum,
                              g.exchange->comm, g.stream), "allreduce(edges)");
-    nccl_check(api.AllReduce(&ctr->changed, &ctr->changed, 2, ncclUint32, ncclSum,
+    static_assert(offsetof(IterCounters, empty_active) == offsetof(IterCounters, changed) + 8 &&
+                      offsetof(IterCounters, bad_min) == offsetof(IterCounters, changed) + 12,
+                  "counter layout: [u64 x2][u32 sums x3][u32 min]");
+    nccl_check(api.AllReduce(&ctr->changed, &ctr->changed, 3, ncclUint32, ncclSum,
                              g.exchange->comm, g.stream), "allreduce(changed)");
     nccl_check(api.AllReduce(&ctr->bad_min, &ctr->bad_min, 1, ncclUint32, ncclMin,
                              g.exchange->comm, g.stream), "allreduce(bad)");

@@ -4,6 +4,14 @@
 // HBM layout per rank (local = owned destination range [v_begin, v_end)),
 // see DESIGN.md §3:
 //   off      u64[nloc+1]        local in-edge offsets (rebased to 0)
+//   vid_of_p u32[nloc]          POSITION order of the local vertices: the R
+//                               vertices with in-edges ("rows", vertex order)
+//                               first, then the in-degree-0 ones. Per-vertex run
+//                               state (property, status, accumulators, the
+//                               sparsified offsets) is stored by position, so
+//                               the vertex epilogue walks the rows densely and
+//                               skips the in-degree-0 tail once none is active.
+//   slot_p, deg_p               message slot / out-degree by position
 //   src      u32[pad+e_loc+..]  in-edge sources as MESSAGE SLOT ids, at padded
 //                               positions pad + local edge (pad = global pos mod 512)
 //   w        W[...]             none | u32 | f32 | f64, padded likewise
@@ -70,10 +78,13 @@ struct Workspace {
 
 // Edge-centric layout of one list (full or sparsified CSC): padded
 // positions P = pad + local edge index, runs of 16 and tasks of 512 padded
-// positions, run_v[r] = local vertex containing the first valid position of
-// run r (see kernels.cuh).
+// positions, run_i[r] = the non-empty vertex containing the first valid
+// position of run r (see kernels.cuh).
 // The edge kernel walks only the list's NON-EMPTY vertices (nz_vid / nz_start,
 // a doubly-compressed view), so long stretches of empty vertices cost nothing.
+// Full list: nz_vid[i] = the local vertex of row i (rows are its non-empty
+// vertices, so row = nz index). Sparsified list: nz_vid[i] = the ROW of its
+// i-th non-empty vertex (the layout runs in row space).
 struct ListMeta {
     uint64_t pad = 0;      // padded position of local edge 0 (global position mod 512)
     uint64_t e = 0;        // local edges
@@ -110,6 +121,11 @@ struct DevGraph {
     // slot range, the only messages any gather reads; exchange_slices)
     std::vector<uint64_t> gathered_slots;
     ListMeta full;
+    // position order (graph.cuh header): rows = full.nz non-empty vertices
+    uint64_t nrows = 0;
+    uint32_t* vid_of_p = nullptr;  // [nloc + 1] local vertex of position p (full.nz_vid = rows)
+    uint32_t* slot_p = nullptr;    // [nloc + 1] message slot of position p
+    uint32_t* deg_p = nullptr;     // [nloc + 1] out-degree of position p
     // gg_dev_graph_create_for_run: the bitmap / compacted sources of
     // sparsify(sigma, seed) are already in the workspace for the next run
     bool pre_sparse = false;
@@ -174,6 +190,9 @@ void export_sources(const DevGraph& g, uint32_t* host_out);
 // Size `meta` for (pad, e) and build its run -> vertex map from `off`.
 void build_runs(DevGraph& g, const uint64_t* off, uint64_t pad, uint64_t e,
                 const std::string& tag, ListMeta& meta);
+// The full list's layout plus the position order (vid_of_p, slot_p, deg_p;
+// needs slot_of and outdeg); every graph constructor ends with it.
+void build_full(DevGraph& g);
 // engine.cpp:63-75 as the integer test mix64(key ^ e) < T (keep_all: sigma >= 1)
 struct SparsifySpec {
     uint64_t T = 0, key = 0;
@@ -197,8 +216,7 @@ uint64_t sparse_pad(DevGraph& g, uint64_t kept_local);
 // engine.cpp:63-75 sparsify into a bitmap over local edges (global ids hashed).
 void sparsify_bitmap(DevGraph& g, uint32_t* bitmap, double sigma, uint64_t seed, bool all_ones);
 // Deferred superstep bad-vertex scan.
-void launch_superstep_invalid(DevGraph& g, const uint8_t* st_cur, const uint8_t* st_next,
-                              const uint64_t* s_off, void* ctr);
+void launch_superstep_invalid(DevGraph& g, const uint8_t* st, const uint64_t* s_off, void* ctr);
 int occupancy_grid(const void* kernel, int block, size_t smem, int num_sms);
 
 }  // namespace ggb

@@ -294,7 +294,7 @@ gg_status gg_dev_graph_load(const char* path, const gg_part_opts* opts, gg_dev_g
             if (hb[1]) fail("graph: out_degree inconsistent with edges");
             if (hb[3]) fail("graph: negative or non-finite weight");
             assign_slots(g);
-            build_runs(g, g.off, g.full.pad, g.e_loc, "full", g.full);
+            build_full(g);
             GGB_CUDA(cudaStreamSynchronize(g.stream));
         } catch (...) {
             delete h;

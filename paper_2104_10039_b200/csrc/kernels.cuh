@@ -40,20 +40,23 @@ namespace ggb {
 enum : int { kModeApprox = GG_MODE_APPROXIMATE, kModeAccurate = GG_MODE_ACCURATE,
              kModeSuperstep = GG_MODE_SUPERSTEP };
 
-// status byte bits (double-buffered per vertex)
+// status byte per position (ONE buffer: an iteration's kernels read the
+// byte before its vertex kernel rewrites it; a skipped vertex's status is
+// already 0, engine.hpp:196, so skipped vertices cost no write)
 constexpr uint8_t kStActive = 1;     // vstatus result (engine.hpp:220)
-constexpr uint8_t kStProcessed = 2;  // processed this iteration (msg buffers differ)
 constexpr uint8_t kStInvalid = 4;    // !valid(fresh) (deferred superstep check)
+constexpr uint8_t kStWasActive = 8;  // superstep: the status before the iteration (engine.hpp:229)
 
 // Per-iteration reductions (engine.hpp:186-189). Field groups are laid out
-// for the multi-GPU allreduce: [u64 sum x2][u32 sum x2][u32 min].
+// for the multi-GPU allreduce: [u64 sum x2][u32 sum x3][u32 min].
 struct IterCounters {
     unsigned long long gathered;
     unsigned long long processed;
     unsigned int changed;
     unsigned int any_invalid;
-    unsigned int bad_min;      // smallest invalid vertex (global id), 0xffffffff = none
-    unsigned int pad;
+    unsigned int empty_active;  // some in-degree-0 vertex ended active (the next
+                                // vertex kernel must walk those positions)
+    unsigned int bad_min;       // smallest invalid vertex (global id), 0xffffffff = none
 };
 
 __global__ void reset_counters_kernel(IterCounters* __restrict__ c, int n);
@@ -91,12 +94,13 @@ struct EdgeArgs {
     const uint32_t* __restrict__ src;       // [padded position]
     const W* __restrict__ w;                // [padded position]
     const uint32_t* __restrict__ run_i;     // [run] non-empty vertex at its first position
-    const uint32_t* __restrict__ nz_vid;    // [nz] local vertex id
+    const uint32_t* __restrict__ nz_row;    // [nz] row of the list's i-th non-empty vertex
+                                            // (nullptr: the full list, row = i)
     const uint64_t* __restrict__ nz_start;  // [nz+1] local edge offset
     uint64_t pad, e_end;                    // valid padded positions [pad, e_end)
     uint64_t ntasks, nruns;
-    const uint64_t* __restrict__ a_off;     // active_in_degree offsets (engine.hpp:154-161)
-    const uint8_t* __restrict__ st_cur;
+    const uint64_t* __restrict__ a_off;     // [R+1] active_in_degree offsets by row (engine.hpp:154-161)
+    const uint8_t* __restrict__ st_cur;     // status by position
     const typename P::Message* __restrict__ msg_cur;  // global ids
     // Message-gather cache classes (hot-first slots: low ids are the most read):
     //   slot < hot_limit: L1 evict_last + L2 evict_last   (register-resident runs)
@@ -105,7 +109,7 @@ struct EdgeArgs {
     uint32_t hot_limit;
     uint32_t l2_limit;
     uint32_t cold_last;
-    typename P::Accum* __restrict__ acc_out;  // [local vertex]
+    typename P::Accum* __restrict__ acc_out;  // [row]
     typename P::Accum* __restrict__ hv;       // [task] continuing head piece
     typename P::Accum* __restrict__ tv;       // [task] continuing tail piece (chain: inclusive)
     // kEdgeChain: per task {state, value} (16-byte slots, accumulators of <= 8
@@ -118,31 +122,37 @@ struct EdgeArgs {
     const IterCounters* stop_if;            // batched iterations: the previous iteration's counters
 };
 
+// Per-vertex run state is indexed by POSITION p (graph.cuh): rows (vertices
+// with in-edges) at [0, nrows), in-degree-0 vertices at [nrows, nloc).
 template <class P, class W>
 struct VertexArgs {
     P prog;
     uint64_t n;
-    uint32_t v_begin, nloc;
-    const uint64_t* __restrict__ off;   // list offsets (unpadded)
+    uint32_t v_begin, nloc, nrows;
+    const uint64_t* __restrict__ off;   // [nrows+1] offsets of the gathered list by row (unpadded)
     uint64_t pad;
-    const uint64_t* __restrict__ a_off;
-    const uint8_t* __restrict__ st_cur;
-    uint8_t* __restrict__ st_next;
-    typename P::Property* __restrict__ prop;          // local vertex ids
-    const typename P::Message* __restrict__ msg_cur;  // message slots
-    typename P::Message* __restrict__ msg_next;
-    const uint32_t* __restrict__ outdeg;              // global ids
-    const uint32_t* __restrict__ slot_of;             // global id -> message slot
-    const typename P::Accum* __restrict__ acc_out;
+    const uint64_t* __restrict__ a_off; // [nrows+1] active_in_degree offsets by row
+    uint8_t* __restrict__ st;                         // status by position
+    typename P::Property* __restrict__ prop;          // by position
+    typename P::Message* __restrict__ msg;            // message slots (one buffer)
+    const uint32_t* __restrict__ vid_of_p;            // local vertex of position p
+    const uint32_t* __restrict__ slot_p;              // message slot of position p
+    const uint32_t* __restrict__ deg_p;               // out-degree of position p
+    const typename P::Accum* __restrict__ acc_out;    // [row]
     const typename P::Accum* __restrict__ hv;
     const typename P::Accum* __restrict__ tv;
     IterCounters* __restrict__ ctr;
     IterCounters* __restrict__ ctr_next;              // reset here for the next iteration
+    const IterCounters* ctr_prev;                     // the previous iteration's (empty_active)
     const IterCounters* stop_if;                      // see EdgeArgs::stop_if
 };
 
-__device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t v) {
-    return (st[v] & kStActive) || a_off[v + 1] > a_off[v];  // engine.hpp:196
+__device__ __forceinline__ bool vertex_processed(const uint8_t* st, const uint64_t* a_off, uint32_t row) {
+    return (st[row] & kStActive) || a_off[row + 1] > a_off[row];  // engine.hpp:196
+}
+template <class P, class W>
+__device__ __forceinline__ uint32_t row_of(const EdgeArgs<P, W>& a, uint64_t i) {
+    return a.nz_row ? a.nz_row[i] : (uint32_t)i;
 }
 
 // Fold loops are fully unrolled (messages stay in registers) unless the
@@ -397,7 +407,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         // skip test of the task's vertices (engine.hpp:196), staged with the
         // starts so the fold does not wait on it at every vertex boundary
         if constexpr (MODE != kEdgePlain)
-            if (j + 1 < cnt) sp0[j] = vertex_processed(a.st_cur, a.a_off, a.nz_vid[i0 + j]) ? 1 : 0;
+            if (j + 1 < cnt) sp0[j] = vertex_processed(a.st_cur, a.a_off, row_of(a, i0 + j)) ? 1 : 0;
     }
     __syncwarp();
     const bool cont = st0[0] < 0;  // the task's first vertex began in an earlier task
@@ -434,7 +444,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                     hvv = x;
                     head_closed = true;
                 } else {
-                    a.acc_out[a.nz_vid[i0 + k]] = x;  // began and ended inside this run
+                    a.acc_out[row_of(a, i0 + k)] = x;  // began and ended inside this run
                 }
                 x = a.prog.gather_identity();
                 ++k;
@@ -487,7 +497,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         if (head_closed) {
             const Accum hval = joins_prev ? a.prog.combine(prevS, hvv) : hvv;
             if (cont && hk == 0) a.hv[t] = hval;
-            else a.acc_out[a.nz_vid[i0 + hk]] = hval;
+            else a.acc_out[row_of(a, i0 + hk)] = hval;
         }
         const int nextLen = __shfl_down_sync(0xffffffffu, len, 1);
         const uint32_t nextHK = __shfl_down_sync(0xffffffffu, (uint32_t)hk, 1);
@@ -497,7 +507,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             const bool first_cont = cont && tk == 0;
             if (first_cont) a.hv[t] = S;
             if (cont_after && !(CHAIN && first_cont)) a.tv[t] = S;
-            else if (!cont_after && !first_cont) a.acc_out[a.nz_vid[i0 + tk]] = S;
+            else if (!cont_after && !first_cont) a.acc_out[row_of(a, i0 + tk)] = S;
             if (CHAIN && cont_after) {  // publish for the tasks this vertex continues into
                 const uint32_t state = first_cont ? kChainPiece : kChainIncl;
                 if constexpr (chain_packed<Accum>()) {
@@ -653,11 +663,16 @@ edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
                                     pol_cold, ht);
 }
 
-// Vertex epilogue: the accumulator of vertex v is acc_out[v] when its list
-// lies inside one task, else tv[t0] (+) hv[t0+1] (+) ... (+) hv[t1] in task
-// order; then GG-Apply, GG-VStatus, valid, message, status, counters.
-// SUPER: after a kEdgeChain superstep tv[t1-1] already holds the
-// left-to-right fold up to task t1-1, so the join is one combine.
+// Vertex epilogue over the POSITIONS: the rows [0, nrows) every iteration,
+// the in-degree-0 tail [nrows, nloc) only while one of them is active (all
+// are at t = 1; an in-degree-0 vertex is processed iff its status is set,
+// engine.hpp:196). The accumulator of row p is acc_out[p] when its list lies
+// inside one task, else tv[t0] (+) hv[t0+1] (+) ... (+) hv[t1] in task order;
+// an in-degree-0 vertex folds nothing (gather_identity). Then GG-Apply,
+// GG-VStatus, valid, message (in place: the iteration's gathers are done),
+// status, counters. Skipped vertices keep property, message and (zero)
+// status: no write. SUPER: after a kEdgeChain superstep tv[t1-1] already
+// holds the left-to-right fold up to task t1-1, so the join is one combine.
 template <class P, class W, bool SUPER>
 __global__ void __launch_bounds__(256)
 vertex_kernel(const VertexArgs<P, W> a) {
@@ -670,40 +685,44 @@ vertex_kernel(const VertexArgs<P, W> a) {
     }
     if (stop_after(a.stop_if)) return;
     unsigned long long g = 0, pcount = 0;
-    unsigned int changed = 0, inv = 0, bad = 0xffffffffu;
-    // U vertices per thread per step, every load of the step issued before
-    // any use (the accumulator of a single-task vertex is read speculatively):
-    // one memory latency per U vertices instead of a dependent chain each.
+    unsigned int changed = 0, inv = 0, bad = 0xffffffffu, eact = 0;
+    const uint32_t pend = __ldg(&a.ctr_prev->empty_active) ? a.nloc : a.nrows;
+    // U positions per thread per step, every load of the step issued before
+    // any use (the accumulator of a single-task row is read speculatively):
+    // one memory latency per U positions instead of a dependent chain each.
     constexpr int U = 2;  // measured on c5: 2 beats 1 (0.90 -> 0.75 ms) and 4 (register pressure)
     const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < a.nloc; base += U * stride) {
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < pend; base += U * stride) {
         uint8_t st[U];
         uint64_t o0[U], o1[U], q0[U], q1[U];
-        uint32_t sv[U], deg[U];
+        uint32_t sv[U], deg[U], lv[U];
         Property prev[U];
         Accum acc1[U];
 #pragma unroll
         for (int i = 0; i < U; ++i) {
-            const uint32_t lv = base + i * stride;
-            if (lv < a.nloc) {
-                const uint32_t v = a.v_begin + lv;
-                sv[i] = a.slot_of[v];
-                st[i] = a.st_cur[lv];
-                o0[i] = a.off[lv];
-                o1[i] = a.off[lv + 1];
-                q0[i] = a.a_off[lv];
-                q1[i] = a.a_off[lv + 1];
-                prev[i] = a.prop[lv];
-                acc1[i] = a.acc_out[lv];
+            const uint32_t p = base + i * stride;
+            if (p < pend) {
+                lv[i] = a.vid_of_p[p];
+                sv[i] = a.slot_p[p];
+                st[i] = a.st[p];
+                prev[i] = a.prop[p];
+                o0[i] = o1[i] = q0[i] = q1[i] = 0;
+                if (p < a.nrows) {
+                    o0[i] = a.off[p];
+                    o1[i] = a.off[p + 1];
+                    q0[i] = a.a_off[p];
+                    q1[i] = a.a_off[p + 1];
+                    acc1[i] = a.acc_out[p];
+                }
                 deg[i] = 0;
-                if constexpr (P::kNeedsDegree) deg[i] = a.outdeg[v];
+                if constexpr (P::kNeedsDegree) deg[i] = a.deg_p[p];
             }
         }
 #pragma unroll
         for (int i = 0; i < U; ++i) {
-            const uint32_t lv = base + i * stride;
-            if (lv >= a.nloc) continue;
-            const uint32_t v = a.v_begin + lv;
+            const uint32_t p = base + i * stride;
+            if (p >= pend) continue;
+            const uint32_t v = a.v_begin + lv[i];
             const bool proc = (st[i] & kStActive) || q1[i] > q0[i];  // engine.hpp:196
             if (proc) {
                 Accum acc = a.prog.gather_identity();
@@ -722,25 +741,24 @@ vertex_kernel(const VertexArgs<P, W> a) {
                 const Property fresh = a.prog.apply(v, acc, prev[i], a.n);  // GG-Apply (:216)
                 const bool active = a.prog.vstatus(prev[i], fresh);         // GG-VStatus (:217)
                 const bool ok = a.prog.valid(fresh);                        // (:218)
-                a.prop[lv] = fresh;
-                a.msg_next[sv[i]] = a.prog.message(fresh, deg[i]);
-                a.st_next[lv] =
-                    (uint8_t)((active ? kStActive : 0) | kStProcessed | (ok ? 0 : kStInvalid));
+                a.prop[p] = fresh;
+                a.msg[sv[i]] = a.prog.message(fresh, deg[i]);
+                a.st[p] = (uint8_t)((active ? kStActive : 0) | (ok ? 0 : kStInvalid) |
+                                    (SUPER && (st[i] & kStActive) ? kStWasActive : 0));
                 g += o1[i] - o0[i];
                 pcount += 1;
                 changed |= active ? 1u : 0u;
+                if (active && p >= a.nrows) eact = 1;
                 if (!ok) {
                     inv = 1;
                     // outside supersteps the reference's scan condition
                     // (status || active_in_degree > 0, engine.hpp:229) is exactly
-                    // "processed"; supersteps are re-checked after the rebuild.
-                    if (!SUPER) bad = min(bad, v);
+                    // "processed"; in a superstep an in-degree-0 vertex's is its
+                    // status (it keeps no edge), rows are re-checked after the rebuild
+                    if (!SUPER || p >= a.nrows) bad = min(bad, v);
                 }
-            } else {
-                // skipped: next = prev (engine.hpp:183), status 0. The message
-                // buffers only differ if the vertex was processed last iteration.
-                if (st[i] & kStProcessed) a.msg_next[sv[i]] = a.msg_cur[sv[i]];
-                a.st_next[lv] = 0;
+            } else if (st[i]) {
+                a.st[p] = 0;  // stale bits of an earlier superstep
             }
         }
     }
@@ -752,21 +770,27 @@ vertex_kernel(const VertexArgs<P, W> a) {
     }
     changed = __reduce_or_sync(0xffffffffu, changed);
     inv = __reduce_or_sync(0xffffffffu, inv);
+    eact = __reduce_or_sync(0xffffffffu, eact);
     bad = __reduce_min_sync(0xffffffffu, bad);
     __shared__ unsigned long long s_g[8], s_p[8];
-    __shared__ unsigned int s_c[8], s_i[8], s_b[8];
+    __shared__ unsigned int s_c[8], s_i[8], s_b[8], s_e[8];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    if (lane == 0) { s_g[wib] = g; s_p[wib] = pcount; s_c[wib] = changed; s_i[wib] = inv; s_b[wib] = bad; }
+    if (lane == 0) {
+        s_g[wib] = g; s_p[wib] = pcount; s_c[wib] = changed; s_i[wib] = inv; s_b[wib] = bad;
+        s_e[wib] = eact;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         const int nw = blockDim.x / 32;
         for (int i = 1; i < nw; ++i) {
             g += s_g[i]; pcount += s_p[i]; changed |= s_c[i]; inv |= s_i[i]; bad = min(bad, s_b[i]);
+            eact |= s_e[i];
         }
         if (g) atomicAdd(&a.ctr->gathered, g);
         if (pcount) atomicAdd(&a.ctr->processed, pcount);
         if (changed) atomicOr(&a.ctr->changed, changed);
         if (inv) atomicOr(&a.ctr->any_invalid, inv);
+        if (eact) atomicOr(&a.ctr->empty_active, eact);
         if (bad != 0xffffffffu) atomicMin(&a.ctr->bad_min, bad);
     }
 }
@@ -774,9 +798,9 @@ vertex_kernel(const VertexArgs<P, W> a) {
 // Superstep bad-vertex rule, engine.hpp:226-233: after the flag rewrite the
 // reference scans (status || active_in_degree > 0) && !valid(next[v]) with
 // active_in_degree already replaced by the kept counts.
-__global__ void superstep_invalid_kernel(uint32_t nloc, uint32_t v_begin,
-                                         const uint8_t* __restrict__ st_cur,
-                                         const uint8_t* __restrict__ st_next,
+__global__ void superstep_invalid_kernel(uint32_t nrows, uint32_t v_begin,
+                                         const uint32_t* __restrict__ vid_of_p,
+                                         const uint8_t* __restrict__ st,
                                          const uint64_t* __restrict__ s_off,
                                          IterCounters* __restrict__ ctr);
 
