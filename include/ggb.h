@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define GGB_ABI_VERSION 4
+#define GGB_ABI_VERSION 5
 
 typedef enum gg_status {
     GG_OK = 0,
@@ -126,7 +126,7 @@ typedef struct gg_run_opts {
 typedef struct gg_pr_params { double damping; double epsilon; } gg_pr_params;      /* :15-40 */
 typedef struct gg_sssp_params { uint32_t source; int32_t graded; } gg_sssp_params; /* :46-83 */
 typedef struct gg_bp_params {                                                      /* :120-145 */
-    int32_t states;             /* 2..4 */
+    int32_t states;             /* 2..64 (2..4 compile-time programs, 5..64 run-time S) */
     double coupling;            /* global coupling (reference BP) */
     double epsilon;
     /* BASELINE C4 extension: when prior_table != NULL the prior comes from the
@@ -170,6 +170,12 @@ typedef struct gg_rmat_params {
 gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* opts,
                                    gg_dev_graph** out, gg_error* err);
 /* Copy the (full, single-rank) CSC back to host buffers (any may be NULL). */
+/* graph.cpp:249-257 symmetrized() of a resident single-rank graph, built on
+ * the device (per destination: its in-edges in order, then its out-edges in
+ * ascending original destination; weights carried); opts may be NULL (same
+ * device, one rank) or place / partition the result like gg_dev_graph_create. */
+gg_status gg_dev_graph_symmetrized(const gg_dev_graph* g, const gg_part_opts* opts,
+                                   gg_dev_graph** out, gg_error* err);
 gg_status gg_dev_graph_export(const gg_dev_graph* g, uint64_t* offsets, uint32_t* sources,
                               void* weights, uint32_t* out_degree);
 /* Binary CSC files straight to HBM (graph.cpp:259-300). Reads the

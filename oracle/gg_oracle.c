@@ -20,8 +20,8 @@
 #endif
 #include <stdint.h>
 
-/* largest property (bytes) the run loops keep on the stack: BP up to 32 states */
-#define OG_MAX_PSIZE 256
+/* largest property (bytes) the run loops keep on the stack: BP up to 64 states */
+#define OG_MAX_PSIZE 512
 
 /* engine.cpp:9-14 (and graph.cpp:22-27, test_support.hpp:12-17) */
 uint64_t og_mix64(uint64_t x) {

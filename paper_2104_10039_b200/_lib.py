@@ -22,7 +22,7 @@ EXPORTS = (
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
     "gg_exchange_nccl_create", "gg_exchange_local_group", "gg_exchange_destroy", "gg_topk_error", "gg_relative_error",
-    "gg_stretch_error",
+    "gg_stretch_error", "gg_dev_graph_symmetrized",
 )
 
 
@@ -62,7 +62,7 @@ class ErrorC(C.Structure):
     _fields_ = [("iteration", C.c_uint64), ("vertex", C.c_uint32), ("msg", C.c_char * 256)]
 
 
-ABI_VERSION = 4  # include/ggb.h GGB_ABI_VERSION
+ABI_VERSION = 5  # include/ggb.h GGB_ABI_VERSION
 
 
 class RunOptsC(C.Structure):
@@ -118,6 +118,7 @@ def lib():
     L.gg_dev_graph_destroy.argtypes = [vp]
     L.gg_dev_graph_info.argtypes = [vp] + [P(C.c_uint64)] * 5
     L.gg_dev_graph_export.argtypes = [vp, vp, vp, vp, vp]
+    L.gg_dev_graph_symmetrized.argtypes = [vp, vp, P(vp), P(ErrorC)]
     L.gg_bp_priors.argtypes = [C.c_uint64, C.c_uint64, vp]
     common = [P(IterRecordC), C.c_uint64, P(RunSummaryC), P(RunOptsC), P(ErrorC)]
     L.gg_run_pr.argtypes = [vp, P(EngineConfigC), P(PrParams), vp] + common

@@ -190,7 +190,10 @@ static gg_status create_impl(const gg_csc_view* csc, const gg_part_opts* opts,
             // upload (one rank; graphs of >= 2^24 edges -- below that the extra
             // launches cost more than the overlap saves): chunks are whole scan
             // tiles, and a chunk's weights travel right after its sources
-            const bool presp = pre && g.nranks == 1 && g.e_loc >= (1ull << 24);
+            // (GGB_PRESPARSE_MIN_EDGES overrides the 2^24 cut, for tests)
+            const char* cut_env = std::getenv("GGB_PRESPARSE_MIN_EDGES");
+            const uint64_t cut = cut_env ? std::strtoull(cut_env, nullptr, 10) : (1ull << 24);
+            const bool presp = pre && g.nranks == 1 && g.e_loc >= cut;
             uint64_t step = (g.e_loc + up.chunk.size() - 1) / std::max<size_t>(up.chunk.size(), 1);
             if (presp) {
                 const uint64_t te = presparse_tile_edges();
@@ -266,6 +269,54 @@ gg_status gg_dev_graph_create_for_run(const gg_csc_view* csc, const gg_part_opts
     return create_impl(csc, opts, &h, sigma, seed, out, err);
 }
 
+}  // extern "C"
+
+namespace ggb {
+// A graph from a full CSC already in HBM (device R-MAT, device
+// symmetrization): one rank adopts the arrays, several ranks copy their
+// slice; then slots, relabel, the full list's layout.
+void adopt_csc(DevGraph& g, RmatCsc r, gg_weight_kind wk) {
+    g.n = r.n;
+    g.e_global = r.e;
+    g.wkind = wk;
+    std::vector<uint64_t> off(r.n + 1);
+    GGB_CUDA(cudaMemcpyAsync(off.data(), r.off, (r.n + 1) * 8, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    finish_graph(g, off.data());
+    g.outdeg = r.outdeg;
+    if (g.nranks == 1) {
+        g.off = r.off;
+        g.src = r.src;
+        g.w = r.w;
+    } else {
+        g.off = static_cast<decltype(g.off)>(dev_alloc((g.nloc + 1) * 8, g.stream));
+        rebase_kernel<<<256, 256, 0, g.stream>>>(r.off + g.v_begin, g.nloc + 1, g.e_base, g.off);
+        GGB_CUDA(cudaGetLastError());
+        const uint64_t pad = g.e_base % kChunkEdges;
+        g.src = static_cast<decltype(g.src)>(dev_alloc((pad + g.e_loc + kRun) * 4, g.stream));
+        GGB_CUDA(cudaMemcpyAsync(g.src + pad, r.src + g.e_base, g.e_loc * 4, cudaMemcpyDeviceToDevice,
+                                 g.stream));
+        const size_t wb = weight_size(g.wkind);
+        if (wb) {
+            g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
+            GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
+                                     static_cast<char*>(r.w) + g.e_base * wb, g.e_loc * wb,
+                                     cudaMemcpyDeviceToDevice, g.stream));
+        }
+        g.full.pad = pad;
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        dev_free(r.off, g.stream);
+        dev_free(r.src, g.stream);
+        if (r.w) dev_free(r.w, g.stream);
+    }
+    assign_slots(g);
+    build_full(g);
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+}
+}  // namespace ggb
+
+extern "C" {
+
 gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* opts,
                                    gg_dev_graph** out, gg_error* err) {
     return guarded(err, [&] {
@@ -274,45 +325,29 @@ gg_status gg_dev_graph_create_rmat(const gg_rmat_params* p, const gg_part_opts* 
         try {
             DevGraph& g = h->g;
             setup_common(g, opts);
-            RmatCsc r = rmat_generate(*p, g.stream);
-            g.n = r.n;
-            g.e_global = r.e;
-            g.wkind = p->weight_kind;
-            std::vector<uint64_t> off(r.n + 1);
-            GGB_CUDA(cudaMemcpyAsync(off.data(), r.off, (r.n + 1) * 8, cudaMemcpyDeviceToHost,
-                                     g.stream));
-            GGB_CUDA(cudaStreamSynchronize(g.stream));
-            finish_graph(g, off.data());
-            g.outdeg = r.outdeg;
-            if (g.nranks == 1) {
-                g.off = r.off;
-                g.src = r.src;
-                g.w = r.w;
-            } else {
-                g.off = static_cast<decltype(g.off)>(dev_alloc((g.nloc + 1) * 8, g.stream));
-                rebase_kernel<<<256, 256, 0, g.stream>>>(r.off + g.v_begin, g.nloc + 1, g.e_base,
-                                                          g.off);
-                GGB_CUDA(cudaGetLastError());
-                const uint64_t pad = g.e_base % kChunkEdges;
-                g.src = static_cast<decltype(g.src)>(dev_alloc((pad + g.e_loc + kRun) * 4, g.stream));
-                GGB_CUDA(cudaMemcpyAsync(g.src + pad, r.src + g.e_base, g.e_loc * 4,
-                                         cudaMemcpyDeviceToDevice, g.stream));
-                const size_t wb = weight_size(g.wkind);
-                if (wb) {
-                    g.w = static_cast<decltype(g.w)>(dev_alloc((pad + g.e_loc + kRun) * wb, g.stream));
-                    GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(g.w) + pad * wb,
-                                             static_cast<char*>(r.w) + g.e_base * wb,
-                                             g.e_loc * wb, cudaMemcpyDeviceToDevice, g.stream));
-                }
-                g.full.pad = pad;
-                GGB_CUDA(cudaStreamSynchronize(g.stream));
-                dev_free(r.off, g.stream);
-                dev_free(r.src, g.stream);
-                if (r.w) dev_free(r.w, g.stream);
-            }
-            assign_slots(g);
-            build_full(g);
-            GGB_CUDA(cudaStreamSynchronize(g.stream));
+            adopt_csc(g, rmat_generate(*p, g.stream), p->weight_kind);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+gg_status gg_dev_graph_symmetrized(const gg_dev_graph* in, const gg_part_opts* opts,
+                                   gg_dev_graph** out, gg_error* err) {
+    return guarded(err, [&] {
+        if (!in || !out) throw Error(GG_INVALID_ARGUMENT, "null argument");
+        if (in->g.nranks != 1) throw Error(GG_INVALID_ARGUMENT, "symmetrized needs a single-rank graph");
+        auto* h = new gg_dev_graph;
+        try {
+            DevGraph& g = h->g;
+            gg_part_opts o{};
+            if (opts) o = *opts;
+            else o.device = in->g.device;
+            if (o.device < 0) o.device = in->g.device;
+            setup_common(g, &o);
+            adopt_csc(g, symmetrize_device(in->g, g.stream), in->g.wkind);
         } catch (...) {
             delete h;
             throw;
@@ -555,12 +590,16 @@ gg_status gg_run_bp(gg_dev_graph* h, const gg_engine_config* cfg, const gg_bp_pa
             default: {
                 if (p->states < 2) throw Error(GG_INVALID_ARGUMENT, "bp states must be >= 2");
                 if (p->states > kBpMaxStates)
-                    throw Error(GG_INVALID_ARGUMENT, "bp states must be <= 16 on device");
-                BeliefPropDyn b;
-                b.states = p->states;
-                b.coupling = p->coupling;
-                b.epsilon = p->epsilon;
-                Engine<BeliefPropDyn, void>::run(g, b, io);
+                    throw Error(GG_INVALID_ARGUMENT, "bp states must be <= 64 on device");
+                auto dyn = [&](auto b) {
+                    b.states = p->states;
+                    b.coupling = p->coupling;
+                    b.epsilon = p->epsilon;
+                    Engine<decltype(b), void>::run(g, b, io);
+                };
+                if (p->states <= 16) dyn(BeliefPropDyn<16>{});
+                else if (p->states <= 32) dyn(BeliefPropDyn<32>{});
+                else dyn(BeliefPropDyn<64>{});
                 break;
             }
         }

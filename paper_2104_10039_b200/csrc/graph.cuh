@@ -173,6 +173,11 @@ struct RmatCsc {
     uint32_t* outdeg = nullptr;
 };
 RmatCsc rmat_generate(const gg_rmat_params& p, cudaStream_t st);
+// graph.cpp:249-257 symmetrized() of a resident single-rank graph, as a full
+// CSC in HBM on `st`'s device (symmetrize.cu)
+RmatCsc symmetrize_device(const DevGraph& g, cudaStream_t st);
+// a DevGraph (after setup_common) from a full device CSC (capi.cu)
+void adopt_csc(DevGraph& g, RmatCsc r, gg_weight_kind wk);
 void bp_priors_device(uint64_t n, uint64_t seed, float* out, cudaStream_t st);
 
 // Hot-first message slots (slot_of / vtx_of_slot) and the rewrite of the

@@ -286,11 +286,13 @@ struct BeliefProp {
 
 // BeliefPropagationProgram with any state count 5..kBpMaxStates chosen at run
 // time (BeliefProp<S> covers 2..4 with compile-time loops); storage is a
-// fixed Belief<kBpMaxStates>, states >= S are never touched. Same formulas
-// and operation order as BeliefProp<S> (algorithms.cpp:9-69).
-constexpr int kBpMaxStates = 16;
+// fixed Belief<MaxS> of the smallest tier (16, 32, 64 states) that holds S,
+// states >= S are never touched. Same formulas and operation order as
+// BeliefProp<S> (algorithms.cpp:9-69).
+constexpr int kBpMaxStates = 64;
+template <int MaxS>
 struct BeliefPropDyn {
-    using Property = Belief<kBpMaxStates>;
+    using Property = Belief<MaxS>;
     using Message = Property;
     using Accum = Property;
     static constexpr bool kMsgIsProp = true;

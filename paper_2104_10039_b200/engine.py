@@ -191,6 +191,15 @@ class DeviceGraph:
         out.weight_dtype = {None: None, "u32": np.uint32, "coupling": np.float32}[weights]
         return out
 
+    def symmetrized(self) -> "DeviceGraph":
+        """graph.cpp:249-257 symmetrized(), built on the device (one rank)."""
+        h = C.c_void_p()
+        err = L.ErrorC()
+        _raise(L.lib().gg_dev_graph_symmetrized(self._h, None, C.byref(h), C.byref(err)), err)
+        out = DeviceGraph(h, self.n, 2 * self.e)
+        out.weight_dtype = getattr(self, "weight_dtype", None)
+        return out
+
     def info(self):
         vals = [C.c_uint64() for _ in range(5)]
         L.lib().gg_dev_graph_info(self._h, *[C.byref(v) for v in vals])

@@ -13,7 +13,10 @@ checkable:
 
 `run_sweep` takes a `runner(graph, program, EngineConfig) -> RunReport`
 (default: the device engine), so the same protocol also drives the CPU
-oracle in the tests.
+oracle in the tests. `plan.graph` may be a host `Graph` (uploaded once) or
+a resident `DeviceGraph` (e.g. a device R-MAT at a BASELINE scale; WCC's
+symmetrized input is then built on the device too), so a sweep at scale
+never moves the graph or any property vector through the host.
 """
 from __future__ import annotations
 
@@ -82,7 +85,8 @@ def _program_and_projection(plan: SweepPlan):  # bench.cpp:269-296
         return (E.sssp_spec(plan.sssp_source, plan.sssp_graded), plan.graph,
                 lambda p: np.asarray(p, np.float64))
     if plan.algo == "wcc":
-        return E.wcc_spec(), symmetrized(plan.graph), lambda p: np.asarray(p, np.float64)
+        g = plan.graph.symmetrized() if isinstance(plan.graph, E.DeviceGraph) else symmetrized(plan.graph)
+        return E.wcc_spec(), g, lambda p: np.asarray(p, np.float64)
     if plan.algo == "bp":
         eps = 1e-6 if plan.epsilon < 0 else plan.epsilon
         return (E.bp_spec(plan.bp_states, plan.bp_coupling, eps), plan.graph,
@@ -142,12 +146,18 @@ def run_sweep(plan: SweepPlan, runner=None) -> list:
         raise ValueError("sweep grids must be non-empty")
     program, graph, project = _program_and_projection(plan)
     n = graph.n
-    dev = None
-    if runner is None:  # device engine: upload the graph once for all cells;
+    dev = owned = None
+    if runner is None:  # device engine: the graph stays resident for all cells;
         # properties stay in HBM and the metric runs on the GPU (metrics.cu)
-        dev = E.DeviceGraph.upload(graph)
+        if isinstance(graph, E.DeviceGraph):
+            dev = graph
+            owned = graph if graph is not plan.graph else None  # a device-built symmetrization
+        else:
+            dev = owned = E.DeviceGraph.upload(graph)
         runner = lambda _g, p, c: E.run(dev, p, c, device_output=True)  # noqa: E731
         project = lambda _p: dev.last_projection()  # noqa: E731
+    elif isinstance(graph, E.DeviceGraph):
+        raise TypeError("a custom runner needs a host Graph")
     metric = plan.metric_override or default_metric(plan.algo)
     k = plan.topk if plan.topk > 0 else max(1, n // 100)
     budget = plan.iterations if plan.iterations > 0 else default_iteration_budget(plan.algo, n)
@@ -187,7 +197,8 @@ def run_sweep(plan: SweepPlan, runner=None) -> list:
     if dev is not None:
         for r in refs:
             r[0].close()
-        dev.close()
+    if owned is not None:
+        owned.close()
     return rows
 
 

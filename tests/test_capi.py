@@ -49,7 +49,7 @@ def test_library_is_sm100a_only():
 def test_abi_version_and_status_strings(ggb):
     from paper_2104_10039_b200 import _lib
     lib = _lib.lib()
-    assert lib.gg_abi_version() == 4
+    assert lib.gg_abi_version() == 5
     assert _lib.status_string(_lib.GG_INVALID_PROPERTY) == "invalid property"
     assert _lib.status_string(99) == "unknown status"
 

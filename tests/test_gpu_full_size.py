@@ -125,3 +125,28 @@ def test_c4_bp_full_scale(ggb, need_reference):
 
 def test_c5_pagerank_full_scale(ggb, need_reference):
     _full(ggb, "c5")
+
+
+def test_c3_wcc_sweep_at_scale_equals_oracle(ggb):
+    """The sweep protocol at BASELINE c3's scale on the device: R-MAT s23
+    resident in HBM, symmetrized there (graph.cpp:249-257), accurate run +
+    sp / gg cells, every cell's accuracy (relative error, bench.cpp:280-287)
+    and edge ratio equal to the oracle-driven sweep on the host copy (which
+    symmetrizes on the host)."""
+    from paper_2104_10039_b200 import sweep
+    from tests.parity import oracle_runner
+    dg = ggb.DeviceGraph.rmat(23, 16, 3)
+    host = dg.to_host()
+    kw = dict(algo="wcc", graph_label="rmat:23,16,3", schemes=["sp", "gg"], sigma_grid=[0.5],
+              theta_grid=[0.0, 0.5], alpha_grid=[4], repeats=1, seeds=[3], threads=THREADS)
+    dev = sweep.run_sweep(sweep.SweepPlan(graph=dg, **kw))
+    orc = sweep.run_sweep(sweep.SweepPlan(graph=host, **kw), runner=oracle_runner)
+    print(sweep.emit_csv(dev, sweep.SweepPlan(graph=host, **kw)))
+    assert len(dev) == len(orc)
+    for x, y in zip(dev, orc):
+        assert (x.scheme, x.sigma, x.theta, x.alpha, x.iters) == (y.scheme, y.sigma, y.theta, y.alpha, y.iters)
+        # relative error: a fixed-order device reduction vs the reference's
+        # left-to-right sum (metrics.cu), equal up to rounding
+        assert x.accuracy == pytest.approx(y.accuracy, rel=1e-12, abs=1e-12), (x, y)
+        assert x.edge_ratio == y.edge_ratio, (x, y)
+    dg.close()

@@ -155,17 +155,18 @@ def test_random_graphs_all_programs(ggb, scheme, seed):
     assert total == 0
 
 
-@pytest.mark.parametrize("states", [4, 5, 8, 16])
+@pytest.mark.parametrize("states", [4, 5, 8, 16, 17, 32, 33, 64])
 def test_bp_many_states(ggb, states):
-    """BeliefProp<S> for S <= 4, the run-time-S program above (any S up to
-    16), against the oracle's reference BP (algorithms.cpp:9-69)."""
+    """BeliefProp<S> for S <= 4, the run-time-S programs above (storage tiers
+    of 16 / 32 / 64 states), against the oracle's reference BP
+    (algorithms.cpp:9-69); S > 64 is rejected with a clear message."""
     g = Oracle.power_law(400, 6.0, 2.1, states)
     for scheme in SCHEMES:
         _, _, mism = compare(ggb, g, BP, scheme=scheme, sigma=0.5, theta=0.01, alpha=3,
                              max_iterations=25, seed=states, states=states, coupling=0.6)
         assert mism == 0
-    with pytest.raises(ValueError, match="<= 16"):
-        ggb.run(to_graph(ggb, g), ggb.BeliefPropagationProgram(17, 0.6, 1e-6),
+    with pytest.raises(ValueError, match="<= 64"):
+        ggb.run(to_graph(ggb, g), ggb.BeliefPropagationProgram(65, 0.6, 1e-6),
                 ggb.EngineConfig(max_iterations=2))
 
 
@@ -437,3 +438,36 @@ def test_weight_ignoring_programs_on_weighted_graphs(ggb, scheme):
     total += compare(ggb, u, WCC, device_weights=u.w.astype(np.uint32), **kw)[2]
     total += compare(ggb, g, BP, device_weights=g.w, **kw)[2]  # S-state BP ignores weights too
     assert total == 0
+
+
+@pytest.mark.parametrize("wkind", ["u32", "f32", "f64"])
+def test_upload_for_run_presparsified_weighted(ggb, monkeypatch, wkind):
+    """The upload-overlapped sparsification on WEIGHTED graphs (weights
+    copied per chunk and compacted with the kept sources): SSSP (u32 / f64
+    distances) and BP with per-edge couplings (f32 weights), uploaded with
+    for_run, equal a plain upload in properties, flags and records. The
+    2^24-edge cut is lowered so small graphs take that path."""
+    monkeypatch.setenv("GGB_PRESPARSE_MIN_EDGES", "1")
+    g = Oracle.power_law(20000, 12.0, 2.1, 5)
+    rng = np.random.default_rng(5)
+    if wkind == "u32":
+        w = rng.integers(1, 255, g.e).astype(np.uint32)
+        prog = ggb.sssp_spec(0, True)
+    elif wkind == "f64":
+        w = rng.uniform(0.1, 3.0, g.e).astype(np.float64)
+        prog = ggb.sssp_spec(0, True)
+    else:
+        w = Oracle.bp_couplings(g.e, 5)
+        prog = ggb.EdgeBeliefPropagationProgram(Oracle.bp_priors(g.n, 5).reshape(-1, 2), 1e-6)
+    graph = ggb.Graph(g.n, g.off, g.src, w, g.outdeg)
+    cfg = ggb.EngineConfig("gg", 0.5, 0.05, 3, 20, 11)
+    plain = ggb.DeviceGraph.upload(graph)
+    ref = ggb.run(plain, prog, cfg, want_flags=True)
+    plain.close()
+    dg = ggb.DeviceGraph.upload(graph, for_run=cfg)  # sparsified during the upload
+    rep = ggb.run(dg, prog, cfg, want_flags=True)
+    dg.close()
+    assert np.array_equal(np.asarray(rep.final_properties).view(np.uint8),
+                          np.asarray(ref.final_properties).view(np.uint8))
+    assert np.array_equal(rep.flags, ref.flags)
+    assert [r.processed_edges for r in rep.per_iteration] == [r.processed_edges for r in ref.per_iteration]
