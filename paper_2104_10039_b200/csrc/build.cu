@@ -232,12 +232,6 @@ void build_full(DevGraph& g) {
 // --------------------------------------------------------------------------
 // bitmap -> sparsified CSC
 // --------------------------------------------------------------------------
-__global__ void popc_kernel(const uint32_t* __restrict__ bitmap, uint64_t nwords,
-                            uint64_t* __restrict__ cnt) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nwords;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        cnt[i] = i < nwords ? (uint64_t)__popc(bitmap[i]) : 0ull;
-}
 
 __device__ __forceinline__ uint64_t bit_rank(const uint32_t* bitmap, const uint64_t* wpref,
                                              uint64_t e) {
@@ -336,9 +330,11 @@ __device__ __forceinline__ uint64_t tile_lookback(unsigned long long* tstate, ui
     return excl;
 }
 
-// Held to 4 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8).
+// Held to 4 / 4 / 3 CTAs per SM (weight bytes 0 / 4 / 8). WB = -1: scan
+// only (flags + per-word prefix + kept total, no compaction) -- several
+// ranks need every rank's kept count before the list's padded base is known.
 template <int WB, bool HASH>
-__global__ void __launch_bounds__(kScanThreads, WB == 0 ? 4 : WB == 4 ? 4 : 3)
+__global__ void __launch_bounds__(kScanThreads, WB <= 0 ? 4 : WB == 4 ? 4 : 3)
 scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w, uint64_t e_loc,
                     uint64_t in_pad, uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_base,
                     SparsifySpec h, uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
@@ -364,7 +360,8 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
         // c5 compaction 2.35 -> 2.18 ms, sparsify + compaction 4.63 -> 4.40
         // ms; one ahead at 6 CTAs, two at 5 and 6, four at 4 and five at 3
         // measured slower)
-        constexpr int D = WB == 0 ? 4 : 2;
+        constexpr bool kCompact = WB >= 0;
+        constexpr int D = WB <= 0 ? 4 : 2;
         uint32_t sv[D][8];
         WT wv[D][8];
         auto load_batch = [&](int k0, uint32_t (&s8)[8], WT (&w8)[8]) {
@@ -373,11 +370,13 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 const uint64_t e = (w0 + k0 + k) * 32 + lane;
                 const bool ine = e < e_loc;
                 s8[k] = ine ? __ldg(src + in_pad + e) : 0u;
-                if constexpr (WB != 0) w8[k] = ine ? __ldg(static_cast<const WT*>(w) + in_pad + e) : WT(0);
+                if constexpr (WB > 0) w8[k] = ine ? __ldg(static_cast<const WT*>(w) + in_pad + e) : WT(0);
             }
         };
+        if constexpr (kCompact) {
 #pragma unroll
-        for (int b = 0; b < D - 1; ++b) load_batch(8 * b, sv[b], wv[b]);
+            for (int b = 0; b < D - 1; ++b) load_batch(8 * b, sv[b], wv[b]);
+        }
         uint32_t word[kScanWPL], off[kScanWPL];  // off: exclusive popcount within the warp
         uint32_t run = 0;
 #pragma unroll
@@ -423,7 +422,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
         }
 #pragma unroll
         for (int b = 0; b < kScanWarpWords / 8; ++b) {
-            if (w0 + 8 * b >= nwords) break;
+            if (!kCompact || w0 + 8 * b >= nwords) break;
             if (b + D - 1 < kScanWarpWords / 8)
                 load_batch(8 * (b + D - 1), sv[(b + D - 1) % D], wv[(b + D - 1) % D]);
 #pragma unroll
@@ -434,7 +433,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 if ((wk >> lane) & 1u) {
                     const uint64_t pos = wbase + ok + (uint32_t)__popc(wk & lt);
                     s_src[pos] = sv[b % D][k];
-                    if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[b % D][k];
+                    if constexpr (WB > 0) static_cast<WT*>(s_w)[pos] = wv[b % D][k];
                 }
             }
         }
@@ -449,7 +448,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
 template <bool HASH>
 static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpec& h,
                                 uint64_t* wpref, uint32_t* s_src, void* s_w, uint64_t tile_lo = 0,
-                                uint64_t tile_hi = ~0ull) {
+                                uint64_t tile_hi = ~0ull, bool scan_only = false) {
     const uint64_t nwords = (g.e_loc + 31) / 32;
     const uint64_t ntiles = (nwords + 1 + kScanTile - 1) / kScanTile;
     if (tile_hi > ntiles) tile_hi = ntiles;
@@ -465,9 +464,14 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     static const int ps0 = per_sm((const void*)scan_compact_kernel<0, HASH>);
     static const int ps4 = per_sm((const void*)scan_compact_kernel<4, HASH>);
     static const int ps8 = per_sm((const void*)scan_compact_kernel<8, HASH>);
-    const int ps = wb == 0 ? ps0 : wb == 4 ? ps4 : ps8;
+    static const int psn = per_sm((const void*)scan_compact_kernel<-1, HASH>);
+    const int ps = scan_only ? psn : wb == 0 ? ps0 : wb == 4 ? ps4 : ps8;
     const uint64_t gr = std::min<uint64_t>(tile_hi - tile_lo, (uint64_t)ps * g.num_sms);
-    if (wb == 0)
+    if (scan_only)
+        scan_compact_kernel<-1, HASH><<<gr, kScanThreads, 0, g.stream>>>(
+            g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
+            ticket, tile_lo, tile_hi);
+    else if (wb == 0)
         scan_compact_kernel<0, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
             ticket, tile_lo, tile_hi);
@@ -656,20 +660,11 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
         return kept;
     }
     // several ranks: the list's padded base needs the kept counts of all
-    // ranks before compaction
-    if (hash) {
-        sparsify_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(
-            bitmap, nwords, g.e_loc, g.e_base, hash->T, hash->key, hash->keep_all);
-        GGB_CUDA(cudaGetLastError());
-        if (launches) ++*launches;
-    }
-    uint64_t* cnt = g.ws.get<uint64_t>("rb.cnt", nwords + 1);
-    popc_kernel<<<grid_for(nwords + 1, 256), 256, 0, g.stream>>>(bitmap, nwords, cnt);
-    GGB_CUDA(cudaGetLastError());
-    size_t tmp = 0;
-    GGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, wpref, nwords + 1, g.stream));
-    void* tmpp = g.ws.get("cub.tmp.rb", tmp);
-    GGB_CUDA(cub::DeviceScan::ExclusiveSum(tmpp, tmp, cnt, wpref, nwords + 1, g.stream));
+    // ranks before compaction: one scan-only pass (flags + word prefix +
+    // kept total), the kept counts exchanged, then the compaction
+    if (hash) launch_scan_compact<true>(g, bitmap, *hash, wpref, s_src, s_w, 0, ~0ull, true);
+    else launch_scan_compact<false>(g, bitmap, SparsifySpec{}, wpref, s_src, s_w, 0, ~0ull, true);
+    if (launches) ++*launches;
     GGB_CUDA(cudaMemcpyAsync(&kept, wpref + nwords, 8, cudaMemcpyDeviceToHost, g.stream));
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     const uint64_t pad = sparse_pad(g, kept);
@@ -689,16 +684,38 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
     }
     build_sparse_layout(g, bitmap, wpref, s_off, pad, kept, meta);
     if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-    if (launches) *launches += 5;
+    if (launches) *launches += 3;
     return kept;
 }
 
 // --------------------------------------------------------------------------
 // hot-first message slots
 // --------------------------------------------------------------------------
+// floor(log2 out-degree) of every vertex (bin 32: out-degree 0)
+__global__ void octave_hist_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
+                                   unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int h[33];
+    for (int i = threadIdx.x; i < 33; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = outdeg[v];
+        atomicAdd(&h[d ? 31 - __clz(d) : 32], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 33; i += blockDim.x)
+        if (h[i]) atomicAdd(hist + i, (unsigned long long)h[i]);
+}
+
+// Slot key: (tier, rank, out-degree class desc); ties keep vertex order
+// (stable radix sort of (key, v)). tier 0 = out-degree octave >= hot_oct
+// (the hot vertices of EVERY rank, a global prefix); with one rank the tier
+// only refines nothing (it is monotone in the class), so the order is (class
+// desc, id).
 __global__ void slot_key_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
-                                const uint64_t* __restrict__ bounds, int nranks,
-                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int qbits) {
+                                const uint64_t* __restrict__ bounds, int nranks, int rank_bits,
+                                int hot_oct, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                int qbits) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t r = 0;
@@ -710,7 +727,8 @@ __global__ void slot_key_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
             const uint32_t frac = qbits ? ((d << (31 - lz)) >> (31 - qbits)) & ((1u << qbits) - 1u) : 0u;
             h = 1u + ((uint32_t)lz << qbits) + frac;
         }
-        keys[v] = (r << 32) | (uint64_t)(0xffffffffu - h);  // rank, then out-degree (class) desc
+        const uint64_t tier = (d && 31 - __clz(d) >= hot_oct) ? 0ull : 1ull;
+        keys[v] = (tier << (32 + rank_bits)) | (r << 32) | (uint64_t)(0xffffffffu - h);
         vals[v] = (uint32_t)v;
     }
 }
@@ -755,17 +773,24 @@ void check_offsets(DevGraph& g, unsigned int* bad) {
     GGB_CUDA(cudaGetLastError());
 }
 
+// per rank: [3r] tier-0 (hot) vertices, [3r+1] out-degree > 0 vertices
 __global__ void gathered_count_kernel(const uint32_t* __restrict__ outdeg, uint64_t n,
-                                      const uint64_t* __restrict__ bounds, int nranks,
+                                      const uint64_t* __restrict__ bounds, int nranks, int hot_oct,
                                       unsigned long long* __restrict__ cnt) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        if (!outdeg[v]) continue;
+        const uint32_t d = outdeg[v];
+        if (!d) continue;
         int r = 0;
         while (r + 1 < nranks && v >= bounds[r + 1]) ++r;
-        atomicAdd(cnt + r, 1ull);
+        if (31 - __clz(d) >= hot_oct) atomicAdd(cnt + 3 * r, 1ull);
+        atomicAdd(cnt + 3 * r + 1, 1ull);
     }
 }
+
+// message slots of the tier-0 (hot) class: the L1+L2 evict_last prefix of an
+// 8-byte message array (engine.cuh hot_bytes, 24 MB)
+constexpr uint64_t kHotTierSlots = (24ull << 20) / 8;
 
 void compute_slots(DevGraph& g) {
     const uint64_t n = g.n;
@@ -783,29 +808,63 @@ void compute_slots(DevGraph& g) {
                              g.stream));
     int qbits = 0;  // octave classes (GGB_SLOT_QBITS: -1 exact degree, q > 0 finer classes)
     if (const char* e = std::getenv("GGB_SLOT_QBITS")) qbits = std::atoi(e);
-    slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, k0, v0, qbits);
-    GGB_CUDA(cudaGetLastError());
     int rank_bits = 0;
     while ((1 << rank_bits) < g.nranks) ++rank_bits;
+    // hot tier (several ranks): the highest out-degree octaves holding at most
+    // kHotTierSlots vertices; one rank: no tier (the class order is already
+    // hot-first)
+    int hot_oct = 33;
+    if (g.nranks > 1) {
+        auto* hist = static_cast<unsigned long long*>(dev_alloc(33 * 8, g.stream));
+        GGB_CUDA(cudaMemsetAsync(hist, 0, 33 * 8, g.stream));
+        octave_hist_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, hist);
+        GGB_CUDA(cudaGetLastError());
+        uint64_t h[33];
+        GGB_CUDA(cudaMemcpyAsync(h, hist, 33 * 8, cudaMemcpyDeviceToHost, g.stream));
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        dev_free(hist, g.stream);
+        uint64_t cum = 0;
+        for (int o = 31; o >= 0; --o) {
+            if (cum + h[o] > kHotTierSlots) break;
+            cum += h[o];
+            hot_oct = o;
+        }
+    }
+    slot_key_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, rank_bits,
+                                                           hot_oct, k0, v0, qbits);
+    GGB_CUDA(cudaGetLastError());
+    const int key_bits = 32 + rank_bits + (g.nranks > 1 ? 1 : 0);
     size_t tmp = 0;
-    GGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
-                                             g.stream));
+    GGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k0, k1, v0, v1, n, 0, key_bits, g.stream));
     void* tmpp = nullptr;
     tmpp = static_cast<decltype(tmpp)>(dev_alloc(tmp, g.stream));
-    GGB_CUDA(cub::DeviceRadixSort::SortPairs(tmpp, tmp, k0, k1, v0, v1, n, 0, 32 + rank_bits,
-                                             g.stream));
+    GGB_CUDA(cub::DeviceRadixSort::SortPairs(tmpp, tmp, k0, k1, v0, v1, n, 0, key_bits, g.stream));
     slot_fill_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(v1, n, g.slot_of, g.vtx_of_slot);
     GGB_CUDA(cudaGetLastError());
-    if (g.nranks > 1) {  // per-rank gathered-slot counts for the message exchange
-        auto* cnt = static_cast<unsigned long long*>(dev_alloc(8 * g.nranks, g.stream));
-        GGB_CUDA(cudaMemsetAsync(cnt, 0, 8 * g.nranks, g.stream));
-        gathered_count_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, g.nranks, cnt);
+    if (g.nranks > 1) {  // per-rank slot ranges of the messages the exchange carries
+        const int R = g.nranks;
+        auto* cnt = static_cast<unsigned long long*>(dev_alloc(8 * 3 * R, g.stream));
+        GGB_CUDA(cudaMemsetAsync(cnt, 0, 8 * 3 * R, g.stream));
+        gathered_count_kernel<<<grid_for(n, 256), 256, 0, g.stream>>>(g.outdeg, n, db, R, hot_oct, cnt);
         GGB_CUDA(cudaGetLastError());
-        g.gathered_slots.assign(g.nranks, 0);
-        GGB_CUDA(cudaMemcpyAsync(g.gathered_slots.data(), cnt, 8 * g.nranks, cudaMemcpyDeviceToHost,
-                                 g.stream));
+        std::vector<uint64_t> c(3 * R);
+        GGB_CUDA(cudaMemcpyAsync(c.data(), cnt, 8 * 3 * R, cudaMemcpyDeviceToHost, g.stream));
         GGB_CUDA(cudaStreamSynchronize(g.stream));
         dev_free(cnt, g.stream);
+        uint64_t hot_total = 0;
+        for (int r = 0; r < R; ++r) hot_total += c[3 * r];
+        g.hot_slots = hot_total;
+        g.gather_ranges.assign(4 * R, 0);
+        uint64_t hb = 0, cb = hot_total;
+        for (int r = 0; r < R; ++r) {
+            const uint64_t nv = g.bounds[r + 1] - g.bounds[r], hot = c[3 * r], gat = c[3 * r + 1];
+            g.gather_ranges[4 * r + 0] = hb;
+            g.gather_ranges[4 * r + 1] = hb + hot;
+            g.gather_ranges[4 * r + 2] = cb;
+            g.gather_ranges[4 * r + 3] = cb + (gat - hot);
+            hb += hot;
+            cb += nv - hot;
+        }
     }
     dev_free(k0, g.stream); dev_free(k1, g.stream); dev_free(v0, g.stream); dev_free(v1, g.stream); dev_free(db, g.stream); dev_free(tmpp, g.stream);
 }

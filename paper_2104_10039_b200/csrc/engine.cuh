@@ -131,11 +131,11 @@ struct Engine {
         const uint64_t be = 4 + sizeof(Msg) + (uint64_t)weight_bytes<W>();
         return edges * be + (super ? edges / 8 : 0);
     }
-    static uint64_t vertex_bytes(uint64_t nloc) {
+    static uint64_t vertex_bytes(uint64_t positions) {
         uint64_t bv = 8 + 2 + 2 * sizeof(Prop) + (P::kMsgIsProp ? 0 : sizeof(Msg)) +
                       (P::kNeedsDegree ? 4 : 0);
         if constexpr (requires { P::kReadsPrior; }) bv += 8;
-        return nloc * bv;
+        return positions * bv;
     }
 
     // shared-memory hot-slot table of edge_kernel_hot (GGB_SMEM_HOT_KB, default
@@ -233,7 +233,6 @@ struct Engine {
         void* s_w = nullptr;
         ListMeta sp;
         cudaEvent_t e4 = timing ? g.event(4) : nullptr, e5 = timing ? g.event(5) : nullptr;
-        cudaEvent_t e6 = timing ? g.event(6) : nullptr, e7 = timing ? g.event(7) : nullptr;
 
         init_kernel<P><<<grid1d(std::max<uint64_t>(n, nloc)), 256, 0, g.stream>>>(
             prog, n, (uint32_t)g.v_begin, (uint32_t)nloc, g.outdeg, g.slot_of, g.vid_of_p, msg, prop, st);
@@ -256,33 +255,37 @@ struct Engine {
         }
         g.pre_sparse = false;  // one run uses it (its supersteps rewrite the bitmap)
         const uint64_t* a_off = sparse ? s_off : g.full.nz_start;  // by row
-        // the hottest message slots (lowest ids: hot-first layout) are pinned in
-        // L2 with evict_last; with several ranks each range has its own hot
-        // prefix and every gather uses evict_normal.
         // Gather cache classes (EdgeArgs::hot_limit). A message array that fits
         // half of L2 is kept there whole; a larger one protects its hottest
-        // prefix in L1 and L2 (measured on c5: 24 MB best of 4..80 MB). With
-        // several ranks the hot vertices are spread over the rank ranges of
-        // the slot order, so no prefix is singled out.
+        // prefix in L1 and L2 (measured on c5: 24 MB best of 4..80 MB). The
+        // hot-first slot order makes the hottest slots a prefix: with one
+        // rank the whole order is by out-degree class; with several, the
+        // tier-0 slots (every rank's highest out-degree octaves, compute_slots)
+        // are the global prefix the classes may use.
+        const uint64_t hot_prefix = g.nranks == 1 ? n : g.hot_slots;
         const bool msgs_fit_l2 = (uint64_t)n * sizeof(Msg) <= (64ull << 20);
-        const uint32_t hot_limit = (g.nranks == 1 && !msgs_fit_l2)
-            ? (uint32_t)std::min<uint64_t>(n, hot_bytes() / sizeof(Msg)) : 0u;
-        // hot slots copied into shared memory by the approximate gather (one
-        // rank: slot order = global heat order)
-        const uint32_t nhot = (kHotOK && g.nranks == 1)
-            ? (uint32_t)std::min<uint64_t>(n, smem_hot_bytes() / sizeof(Msg)) : 0u;
-        const uint32_t l2_limit =
-            g.nranks == 1 ? (uint32_t)std::min<uint64_t>(n, (80ull << 20) / sizeof(Msg)) : 0u;
+        const uint32_t hot_limit = !msgs_fit_l2
+            ? (uint32_t)std::min<uint64_t>(hot_prefix, hot_bytes() / sizeof(Msg)) : 0u;
+        // hot slots copied into shared memory by the approximate gather
+        const uint32_t nhot = kHotOK
+            ? (uint32_t)std::min<uint64_t>(hot_prefix, smem_hot_bytes() / sizeof(Msg)) : 0u;
+        const uint32_t l2_limit = (uint32_t)std::min<uint64_t>(hot_prefix, (80ull << 20) / sizeof(Msg));
 
         uint64_t iterations_run = 0, total_edges = 0;
+        bool prev_empty_active = true;  // every status starts active: t = 1 walks every position
         double total_wall = 0.0;
         // Iterations are enqueued in batches: a stretch of consecutive
         // non-superstep iterations (one rank) is launched back to back with
         // device-side early exit (stop_after) and read back with one sync;
         // supersteps and multi-rank iterations form batches of one. Results
         // and records are those of the one-at-a-time loop (engine.hpp:177-241).
+        // Several ranks batch too: every rank enqueues the same iterations,
+        // a stopped iteration's kernels return at once but its exchange still
+        // runs (unchanged messages, zero counters) on every rank, so the
+        // collectives stay matched; NCCL calls are stream-ordered (one host
+        // sync per batch), the in-process transport syncs inside each call.
         auto batchable = [&](uint64_t u) {
-            return g.nranks == 1 && mode_for(cfg.scheme, u, cfg.alpha) != GG_MODE_SUPERSTEP;
+            return mode_for(cfg.scheme, u, cfg.alpha) != GG_MODE_SUPERSTEP;
         };
         bool done = false;
         for (uint64_t t = 1; t <= cfg.max_iterations && !done;) {  // engine.hpp:177
@@ -293,7 +296,7 @@ struct Engine {
             double rb_ms = 0.0;
             bool super = false;
             // timing events of batch member k (single iterations keep e0..e7)
-            auto ev = [&](int k, int i) { return B == 1 ? g.event(i) : g.batch_event(4 * k + i); };
+            auto ev = [&](int k, int i) { return B == 1 ? g.event(i) : g.batch_event(8 * k + i); };
             for (int k = 0; k < B; ++k) {
             const uint64_t u = t + k;
             const int mode = mode_for(cfg.scheme, u, cfg.alpha);
@@ -382,10 +385,10 @@ struct Engine {
                 ++launches;
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
-                if (timing) GGB_CUDA(cudaEventRecord(e6, g.stream));
+                if (timing) GGB_CUDA(cudaEventRecord(ev(k, 6), g.stream));
                 exchange_slices(g, msg, sizeof(Msg), /*slots=*/true);
                 exchange_counters(g, ctr);
-                if (timing) GGB_CUDA(cudaEventRecord(e7, g.stream));
+                if (timing) GGB_CUDA(cudaEventRecord(ev(k, 7), g.stream));
             }
             }  // batch member k
             GGB_CUDA(cudaMemcpyAsync(h_ring, ring, kRing * sizeof(IterCounters),
@@ -426,13 +429,16 @@ struct Engine {
                     r.vertex_ms = timing ? event_ms(ev(k, 1), ev(k, 2)) : 0.0;
                     r.kernel_ms = r.edge_ms + r.vertex_ms;
                     r.rebuild_ms = rb_ms;
-                    r.exchange_ms = (timing && g.nranks > 1) ? event_ms(e6, e7) : 0.0;
+                    r.exchange_ms = (timing && g.nranks > 1) ? event_ms(ev(k, 6), ev(k, 7)) : 0.0;
                     // per-rank algorithmic bytes of this rank's launches
                     const uint64_t local_edges = approx ? kept : g.e_loc;
                     r.edge_bytes = edge_bytes(local_edges, super);
-                    r.vertex_bytes = vertex_bytes(nloc);
+                    // positions the vertex kernel walked: the rows, and the
+                    // in-degree-0 tail when one of them was active (always at t = 1)
+                    r.vertex_bytes = vertex_bytes(prev_empty_active ? nloc : R);
                     r.algo_bytes = r.edge_bytes + r.vertex_bytes;
                 }
+                prev_empty_active = hc.empty_active != 0;
                 iterations_run = u;
                 total_edges += hc.gathered;
                 total_wall += wall;

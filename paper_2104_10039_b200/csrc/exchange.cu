@@ -69,10 +69,17 @@ struct LocalGroup {
     }
 };
 
-// element range of rank r's slice
-static inline void slice_of(const DevGraph& g, int r, bool slots, uint64_t& b, uint64_t& e) {
-    b = g.bounds[r];
-    e = slots && !g.gathered_slots.empty() ? b + g.gathered_slots[r] : g.bounds[r + 1];
+// element ranges of rank r's slice: the vertex range, or (slots) the slot
+// ranges of its gathered messages (graph.cuh gather_ranges)
+static inline int ranges_of(const DevGraph& g, int r, bool slots, uint64_t (&b)[2], uint64_t (&e)[2]) {
+    if (slots && !g.gather_ranges.empty()) {
+        b[0] = g.gather_ranges[4 * r]; e[0] = g.gather_ranges[4 * r + 1];
+        b[1] = g.gather_ranges[4 * r + 2]; e[1] = g.gather_ranges[4 * r + 3];
+        return 2;
+    }
+    b[0] = g.bounds[r];
+    e[0] = g.bounds[r + 1];
+    return 1;
 }
 
 static void local_slices(DevGraph& g, LocalGroup& L, void* buf, size_t elem, bool slots) {
@@ -80,12 +87,15 @@ static void local_slices(DevGraph& g, LocalGroup& L, void* buf, size_t elem, boo
     L.bufs[g.rank] = buf;
     L.barrier();
     for (int r = 0; r < g.nranks; ++r) {
-        uint64_t b, e;
-        slice_of(g, r, slots, b, e);
-        if (r == g.rank || e == b) continue;
-        GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(buf) + b * elem,
-                                 static_cast<const char*>(L.bufs[r]) + b * elem, (e - b) * elem,
-                                 cudaMemcpyDefault, g.stream));
+        if (r == g.rank) continue;
+        uint64_t b[2], e[2];
+        const int k = ranges_of(g, r, slots, b, e);
+        for (int i = 0; i < k; ++i) {
+            if (e[i] == b[i]) continue;
+            GGB_CUDA(cudaMemcpyAsync(static_cast<char*>(buf) + b[i] * elem,
+                                     static_cast<const char*>(L.bufs[r]) + b[i] * elem,
+                                     (e[i] - b[i]) * elem, cudaMemcpyDefault, g.stream));
+        }
     }
     GGB_CUDA(cudaStreamSynchronize(g.stream));
     L.barrier();  // nobody rewrites its buffer while another rank copies from it
@@ -106,12 +116,14 @@ void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots
     const NcclApi& api = nccl();
     nccl_check(api.GroupStart(), "ncclGroupStart");
     for (int r = 0; r < g.nranks; ++r) {
-        uint64_t b, e;
-        slice_of(g, r, slots, b, e);
-        if (e == b) continue;
-        char* p = static_cast<char*>(global_buf) + b * elem_size;
-        nccl_check(api.Broadcast(p, p, (e - b) * elem_size, ncclChar, r, g.exchange->comm, g.stream),
-                   "ncclBroadcast");
+        uint64_t b[2], e[2];
+        const int k = ranges_of(g, r, slots, b, e);
+        for (int i = 0; i < k; ++i) {
+            if (e[i] == b[i]) continue;
+            char* p = static_cast<char*>(global_buf) + b[i] * elem_size;
+            nccl_check(api.Broadcast(p, p, (e[i] - b[i]) * elem_size, ncclChar, r, g.exchange->comm,
+                                     g.stream), "ncclBroadcast");
+        }
     }
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
 }

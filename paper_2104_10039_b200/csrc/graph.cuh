@@ -117,9 +117,13 @@ struct DevGraph {
     // into L2; src arrays hold slot ids. slot_of[v] / vtx_of_slot[s], global.
     uint32_t* slot_of = nullptr;
     uint32_t* vtx_of_slot = nullptr;
-    // per rank: how many of its slots have out-degree > 0 (a prefix of its
-    // slot range, the only messages any gather reads; exchange_slices)
-    std::vector<uint64_t> gathered_slots;
+    // Several ranks: the message slots a gather can read (out-degree > 0) of
+    // each rank's vertices, as two slot ranges per rank {b0, e0, b1, e1}:
+    // its hot tier-0 slots and the out-degree > 0 prefix of its tier-1 slots
+    // (compute_slots); hot_slots = the tier-0 total, a GLOBAL prefix of the
+    // slot order, so every rank's gathers can single it out (L1/L2 classes).
+    std::vector<uint64_t> gather_ranges;
+    uint64_t hot_slots = 0;
     ListMeta full;
     // position order (graph.cuh header): rows = full.nz non-empty vertices
     uint64_t nrows = 0;

@@ -270,8 +270,10 @@ __device__ __forceinline__ void warp_write_flags(uint32_t* __restrict__ bitmap, 
 // waits on a later task: the look-back always completes.
 //
 // Accumulators of up to 32 bytes travel with their state in H = size/8
-// 16-byte halves {state, 8 value bytes}, each written and read with one
-// relaxed vector access (single-copy atomic), so no fence is needed; a slot
+// 16-byte halves {state, 8 value bytes}, each written and read as ONE
+// relaxed .b128 memory operation (single-copy atomic in the PTX memory
+// model; a .v2.u64 access would be two operations there, although both
+// compile to the same STG/LDG.E.128.STRONG.GPU), so no fence is needed; a slot
 // is ready when all its halves carry the same non-zero state (a reader that
 // catches a piece -> inclusive rewrite half way sees mixed states and
 // retries). Larger accumulators are written to hv / tv and published by a
@@ -287,8 +289,8 @@ __device__ __forceinline__ void chain_put(ulonglong2* d, uint32_t state, const A
     unsigned long long bits[H] = {};
     memcpy(bits, &v, sizeof(Accum));
 #pragma unroll
-    for (int h = 0; h < H; ++h)
-        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};"
+    for (int h = 0; h < H; ++h)  // one 128-bit memory operation (.b128: single-copy atomic)
+        asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.gpu.global.b128 [%0], t; }"
                      :: "l"(d + h), "l"((unsigned long long)state), "l"(bits[h]) : "memory");
 }
 template <class Accum>
@@ -297,7 +299,7 @@ __device__ __forceinline__ uint32_t chain_get(const ulonglong2* d, Accum& v) {
     unsigned long long st[H], bits[H];
 #pragma unroll
     for (int h = 0; h < H; ++h)
-        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+        asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
                      : "=l"(st[h]), "=l"(bits[h]) : "l"(d + h) : "memory");
     memcpy(&v, bits, sizeof(Accum));
     bool same = true;

@@ -471,3 +471,26 @@ def test_upload_for_run_presparsified_weighted(ggb, monkeypatch, wkind):
                           np.asarray(ref.final_properties).view(np.uint8))
     assert np.array_equal(rep.flags, ref.flags)
     assert [r.processed_edges for r in rep.per_iteration] == [r.processed_edges for r in ref.per_iteration]
+
+
+@pytest.mark.parametrize("prog", ["pr", "bp5"])
+def test_chain_stress_bitwise(ggb, prog):
+    """The superstep chain's carries and the look-back scans do not depend on
+    timing: 24 runs over grids from 1 CTA to the default (different warps
+    hold different tasks, predecessors finish in different orders) are
+    bit-identical in properties, flags and counts. Hub-heavy graph: in-lists
+    spanning many 512-edge tasks. (compute-sanitizer is closed on this pool;
+    this and the grid-invariance tests stand in for racecheck.)"""
+    g = Oracle.power_law(30000, 40.0, 1.8, 11)
+    program = ggb.pagerank_spec() if prog == "pr" else ggb.bp_spec(5, 0.7)
+    dg = ggb.DeviceGraph.upload(to_graph(ggb, g))
+    cfg = ggb.EngineConfig("gg", 0.5, 0.01, 1, 12, 3)  # a superstep every other iteration
+    base = ggb.run(dg, program, cfg, want_flags=True)
+    assert sum(r.mode == ggb.IterationMode.superstep for r in base.per_iteration) >= 3
+    for k, grid in enumerate([1, 2, 5, 37, 148, 0] * 4):
+        r = ggb.run(dg, program, cfg, want_flags=True, grid_ctas=grid)
+        assert np.array_equal(np.asarray(r.final_properties).view(np.uint8),
+                              np.asarray(base.final_properties).view(np.uint8)), (k, grid)
+        assert np.array_equal(r.flag_words, base.flag_words), (k, grid)
+        assert [x.active_vertices for x in r.per_iteration] == [x.active_vertices for x in base.per_iteration]
+    dg.close()
