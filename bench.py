@@ -265,7 +265,7 @@ def summarize(args, wl, reps, info, e, per_rank_frac, peak_info):
     return roofline, gteps(approx), gteps(full), per
 
 
-def exchange_stats(ggb, wl, world, per, host_out_degree, bounds):
+def exchange_stats(ggb, wl, world, per, host_out_degree, bounds, fused=False):
     """NVLink bytes each rank receives per iteration (the gathered message
     slots of the other ranks' ranges) and the measured
     exchange time per iteration (CUDA events around it, this rank)."""
@@ -279,7 +279,11 @@ def exchange_stats(ggb, wl, world, per, host_out_degree, bounds):
     ex = [it.exchange_ms for it in per if it.exchange_ms]
     return {"bytes_received_per_iter_per_rank": recv, "max_bytes_received_per_iter": max(recv),
             "exchange_ms_per_iter_rank0": round(sum(ex) / len(ex), 4) if ex else None,
-            "what": "message slots with out-degree > 0 of the other ranks' ranges, AllGatherV"}
+            "what": "message slots with out-degree > 0 of the other ranks' ranges",
+            "path": ("fused: the vertex kernel stores them into every rank's replica (peer "
+                     "memory), one barrier between gathers and vertex kernels; exchange_ms = "
+                     "the counter all-reduce" if fused else
+                     "all-gather after the vertex kernel (grouped ncclBroadcast = AllGatherV)")}
 
 
 def ours(args):
@@ -300,6 +304,7 @@ def ours(args):
         uid = [ggb.Exchange.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         exchange = ggb.Exchange(rank, world, uid[0])
+        exchange.set_fused(not args.no_fused)
     wl = WORKLOADS[args.workload]
     t_setup = time.perf_counter()
     dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],
@@ -414,7 +419,7 @@ def ours(args):
     xstats = None
     if world > 1:
         xstats = exchange_stats(ggb, wl, world, per, host.out_degree,
-                                ggb.partition_plan(host, world))
+                                ggb.partition_plan(host, world), reps[0].exchange_fused)
 
     # ---- reference CPU path beside it (rank 0, N=1 only), bounded sample
     cpu = None
@@ -437,6 +442,15 @@ def ours(args):
         "accuracy": accuracy,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk,
+        # per iteration of one run: processed edges / vertices (engine.hpp:186-189,
+        # `active_vertices` = the vertices that passed the skip test) and the
+        # edge / vertex kernel times (CUDA events, engine stream)
+        "per_iteration": [{"mode": it.mode.name, "edges": it.processed_edges,
+                           "vertices": it.active_vertices,
+                           "vertex_frac": round(it.active_vertices / n, 4) if n else None,
+                           "edge_ms": round(it.edge_ms, 3), "vertex_ms": round(it.vertex_ms, 3),
+                           "rebuild_ms": round(it.rebuild_ms, 3)}
+                          for it in reps[0].per_iteration],
     }
     if xstats:
         out["exchange"] = xstats
@@ -462,6 +476,8 @@ def ours_local(args):
     wl = WORKLOADS[args.workload]
     torch.cuda.set_device(0)
     xs = ggb.Exchange.local_group(N)
+    for x in xs:
+        x.set_fused(not args.no_fused)
     create_lock = threading.Lock()
     res = [None] * N
     errs = []
@@ -512,7 +528,8 @@ def ours_local(args):
     bounds = [0]
     for r in res:
         bounds.append(r["info"]["v_end"])
-    xstats = exchange_stats(ggb, wl, N, per, res[0]["od"], np.array(bounds, np.uint64))
+    xstats = exchange_stats(ggb, wl, N, per, res[0]["od"], np.array(bounds, np.uint64),
+                            res[0]["reps"][0].exchange_fused)
     xstats["exchange_ms_per_iter_per_rank"] = [
         round(sum(it.exchange_ms for rep in r["reps"] for it in rep.per_iteration) /
               max(1, sum(len(rep.per_iteration) for rep in r["reps"])), 4) for r in res]
@@ -742,6 +759,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c5")
     ap.add_argument("--transport", choices=["nccl", "local"], default="nccl")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="N > 1: all-gather the messages after the vertex kernel instead of the "
+                         "fused peer-memory stores")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true", help="reference arm: skip its accuracy runs")

@@ -105,6 +105,8 @@ typedef struct gg_run_summary {
     double total_wall_seconds;
     uint64_t kept_edges;        /* active edges after the run (flag popcount) */
     uint32_t kernel_launches;   /* our kernels launched by this run */
+    uint32_t exchange_fused;    /* several ranks: 1 = messages stored into the peer replicas
+                                   by the vertex kernel, 0 = all-gathered after it */
 } gg_run_summary;
 
 typedef struct gg_error {
@@ -237,6 +239,13 @@ gg_status gg_exchange_nccl_create(const uint8_t unique_id[128], int rank, int nr
  * host barriers + device copies. For single-GPU validation of the partitioned
  * engine and for multi-tenant hosts. Destroy each handle. */
 gg_status gg_exchange_local_group(int nranks, gg_exchange** out);
+/* Fused exchange on (default) or off. On: the vertex kernel stores every new
+ * message into each rank's replica (peer memory over NVLink; CUDA IPC maps the
+ * replicas of the NCCL transport), with one barrier per iteration between the
+ * gathers and the vertex kernels. Off, or when some rank cannot map its peers:
+ * the messages are all-gathered after the vertex kernel (grouped
+ * ncclBroadcast). Set the same value on every rank before a run. */
+gg_status gg_exchange_set_fused(gg_exchange* x, int on);
 gg_status gg_exchange_destroy(gg_exchange* x);
 
 /* Host metrics (metrics.cpp:60-113); accuracy = (1 - err) * 100. */

@@ -21,7 +21,7 @@ EXPORTS = (
     "gg_dev_graph_info", "gg_dev_graph_create_rmat", "gg_dev_graph_export", "gg_bp_priors",
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
-    "gg_exchange_nccl_create", "gg_exchange_local_group", "gg_exchange_destroy", "gg_topk_error", "gg_relative_error",
+    "gg_exchange_nccl_create", "gg_exchange_local_group", "gg_exchange_destroy", "gg_exchange_set_fused", "gg_topk_error", "gg_relative_error",
     "gg_stretch_error", "gg_dev_graph_symmetrized",
 )
 
@@ -55,7 +55,7 @@ class IterRecordC(C.Structure):
 class RunSummaryC(C.Structure):
     _fields_ = [("iterations_run", C.c_uint64), ("total_processed_edges", C.c_uint64),
                 ("total_wall_seconds", C.c_double), ("kept_edges", C.c_uint64),
-                ("kernel_launches", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("exchange_fused", C.c_uint32)]
 
 
 class ErrorC(C.Structure):
@@ -147,6 +147,7 @@ def lib():
     L.gg_nccl_unique_id.argtypes = [vp]
     L.gg_exchange_nccl_create.argtypes = [vp, C.c_int, C.c_int, P(vp), P(ErrorC)]
     L.gg_exchange_destroy.argtypes = [vp]
+    L.gg_exchange_set_fused.argtypes = [vp, C.c_int]
     L.gg_exchange_local_group.argtypes = [C.c_int, P(vp)]
     L.gg_topk_error.argtypes = [vp, vp, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.gg_relative_error.argtypes = [vp, vp, C.c_uint64, P(C.c_double)]

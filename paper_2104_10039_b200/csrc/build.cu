@@ -923,6 +923,8 @@ void launch_superstep_invalid(DevGraph& g, const uint8_t* st, const uint64_t* s_
 }
 
 DevGraph::~DevGraph() {
+    exchange_release_peers(*this);
+    if (ipc_msg) cudaFree(ipc_msg);
     ws.release();
     if (h_ctr) cudaFreeHost(h_ctr);
     for (cudaEvent_t e : ev)

@@ -199,9 +199,11 @@ struct Engine {
         const unsigned cap = io.opts ? io.opts->grid_ctas : 0u;
 
         // one message buffer: an iteration's gathers complete before its
-        // vertex kernel rewrites the messages (same stream); per-vertex state
-        // by position (graph.cuh)
-        Msg* msg = ws.get<Msg>("msg", n);
+        // vertex kernel rewrites the messages (same stream; several ranks with
+        // the fused exchange: a barrier, since the vertex kernels also write
+        // the other ranks' replicas); per-vertex state by position (graph.cuh)
+        Msg* msg = static_cast<Msg*>(exchange_msg_buffer(g, n * sizeof(Msg)));
+        const bool fused = exchange_register_peers(g, msg, n * sizeof(Msg));
         Prop* prop = ws.get<Prop>("prop", nloc + 1);
         uint8_t* st = ws.get<uint8_t>("st", nloc + 1);
         const uint64_t R = g.nrows;
@@ -330,6 +332,11 @@ struct Engine {
             }
             ea.bitmap = bitmap;
             ea.theta = cfg.theta;
+            {
+                const bool normal = cfg.theta > 0x1p-900 && cfg.theta < 0x1p+900;
+                ea.theta_hi = normal ? cfg.theta * (1.0 + 0x1p-40) : std::nan("");
+                ea.theta_lo = normal ? cfg.theta * (1.0 - 0x1p-40) : std::nan("");
+            }
             ea.stop_if = k ? ring + (u - 1) % kRing : nullptr;
             VertexArgs<P, W> va{};
             va.prog = prog;
@@ -350,6 +357,14 @@ struct Engine {
             va.hv = hv;
             va.tv = tv;
             IterCounters* ctr = ring + u % kRing;
+            va.npeers = 0;
+            if (fused) {
+                va.npeers = g.nranks;
+                va.self = g.rank;
+                for (int r = 0; r < g.nranks; ++r) va.peers[r] = static_cast<Msg*>(g.peer_msg[r]);
+                const uint64_t* gr = g.gather_ranges.data() + 4 * g.rank;
+                va.gb0 = gr[0]; va.ge0 = gr[1]; va.gb1 = gr[2]; va.ge1 = gr[3];
+            }
             va.ctr = ctr;
             va.ctr_next = ring + (u + 1) % kRing;
             va.ctr_prev = ring + (u - 1) % kRing;  // u = 1: slot 0 = "all statuses active"
@@ -371,8 +386,19 @@ struct Engine {
                 ++launches;
             }
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 1), g.stream));
-            if (super) vertex_kernel<P, W, true><<<capped(grid1d(nloc), cap), 256, 0, g.stream>>>(va);
-            else vertex_kernel<P, W, false><<<capped(grid1d(nloc), cap), 256, 0, g.stream>>>(va);
+            // fused exchange: every rank's gathers are done before any vertex
+            // kernel writes the replicas
+            if (fused) exchange_barrier(g);
+            {
+                const unsigned vg = capped(grid1d(nloc), cap);
+                if (fused) {
+                    if (super) vertex_kernel<P, W, true, true><<<vg, 256, 0, g.stream>>>(va);
+                    else vertex_kernel<P, W, false, true><<<vg, 256, 0, g.stream>>>(va);
+                } else {
+                    if (super) vertex_kernel<P, W, true><<<vg, 256, 0, g.stream>>>(va);
+                    else vertex_kernel<P, W, false><<<vg, 256, 0, g.stream>>>(va);
+                }
+            }
             GGB_CUDA(cudaGetLastError());
             ++launches;
             if (timing) GGB_CUDA(cudaEventRecord(ev(k, 2), g.stream));
@@ -386,7 +412,7 @@ struct Engine {
             }
             if (g.nranks > 1) {  // property exchange + counter allreduce
                 if (timing) GGB_CUDA(cudaEventRecord(ev(k, 6), g.stream));
-                exchange_slices(g, msg, sizeof(Msg), /*slots=*/true);
+                if (!fused) exchange_slices(g, msg, sizeof(Msg), /*slots=*/true);
                 exchange_counters(g, ctr);
                 if (timing) GGB_CUDA(cudaEventRecord(ev(k, 7), g.stream));
             }
@@ -500,6 +526,7 @@ struct Engine {
             io.sum->total_wall_seconds = total_wall;
             io.sum->kept_edges = kept;
             io.sum->kernel_launches = (uint32_t)launches;
+            io.sum->exchange_fused = fused ? 1u : 0u;
         }
     }
 };

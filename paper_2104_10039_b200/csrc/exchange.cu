@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <condition_variable>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -153,6 +154,144 @@ static std::vector<uint64_t> exchange_all(DevGraph& g, uint64_t local) {
     return h;
 }
 
+// every rank's n bytes, in rank order (setup only)
+static std::vector<uint8_t> exchange_all_bytes(DevGraph& g, const void* mine, size_t n) {
+    std::vector<uint8_t> out(g.nranks * n);
+    if (g.exchange && g.exchange->local) {
+        LocalGroup& L = *g.exchange->local;
+        L.bufs[g.rank] = const_cast<void*>(mine);
+        L.barrier();
+        for (int r = 0; r < g.nranks; ++r) std::memcpy(out.data() + r * n, L.bufs[r], n);
+        L.barrier();
+        return out;
+    }
+    const NcclApi& api = nccl();
+    uint8_t* d = g.ws.get<uint8_t>("xbytes", g.nranks * n);
+    GGB_CUDA(cudaMemcpyAsync(d + g.rank * n, mine, n, cudaMemcpyHostToDevice, g.stream));
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int r = 0; r < g.nranks; ++r)
+        nccl_check(api.Broadcast(d + r * n, d + r * n, n, ncclChar, r, g.exchange->comm, g.stream),
+                   "ncclBroadcast(bytes)");
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    GGB_CUDA(cudaMemcpyAsync(out.data(), d, g.nranks * n, cudaMemcpyDeviceToHost, g.stream));
+    GGB_CUDA(cudaStreamSynchronize(g.stream));
+    return out;
+}
+
+// true on every rank iff `ok` on every rank
+static bool exchange_all_true(DevGraph& g, bool ok) {
+    for (uint64_t v : exchange_all(g, ok ? 1 : 0))
+        if (!v) return false;
+    return true;
+}
+
+void exchange_release_peers(DevGraph& g) {
+    for (void* p : g.ipc_opened) cudaIpcCloseMemHandle(p);
+    g.ipc_opened.clear();
+    g.peer_msg.clear();
+    g.peer_msg_for = nullptr;
+    g.peer_msg_bytes = 0;
+}
+
+void* exchange_msg_buffer(DevGraph& g, size_t bytes) {
+    if (g.nranks > 1 && g.exchange && g.exchange->comm && g.exchange->fused) {
+        if (g.ipc_msg_bytes < bytes) {
+            // every rank grows its buffer in the same run (same n, same
+            // message type), and re-registers its peers before the run uses them
+            exchange_release_peers(g);
+            if (g.ipc_msg) GGB_CUDA(cudaFree(g.ipc_msg));
+            g.ipc_msg = nullptr;
+            GGB_CUDA(cudaMalloc(&g.ipc_msg, bytes ? bytes : 16));
+            g.ipc_msg_bytes = bytes;
+        }
+        return g.ipc_msg;
+    }
+    return g.ws.get("msg", bytes);
+}
+
+bool exchange_register_peers(DevGraph& g, void* msg, size_t bytes) {
+    if (g.nranks <= 1 || !g.exchange) return false;
+    if (!g.peer_msg.empty() && g.peer_msg_for == msg && g.peer_msg_bytes >= bytes) return true;
+    exchange_release_peers(g);
+    // every step ends in an agreement round: all ranks take the same path
+    const bool want = g.exchange->fused && g.nranks <= kMaxPeers;
+    if (!exchange_all_true(g, want)) return false;
+    std::vector<void*> ptrs(g.nranks, nullptr);
+    bool ok = true;
+    if (g.exchange->local) {
+        GGB_CUDA(cudaStreamSynchronize(g.stream));  // init writes of this rank's replica
+        struct Rec { void* p; int device; };
+        const Rec mine{msg, g.device};
+        const std::vector<uint8_t> all = exchange_all_bytes(g, &mine, sizeof(Rec));
+        for (int r = 0; r < g.nranks; ++r) {
+            Rec x;
+            std::memcpy(&x, all.data() + r * sizeof(Rec), sizeof(Rec));
+            ptrs[r] = x.p;
+            if (x.device == g.device) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, g.device, x.device) != cudaSuccess || !can) {
+                cudaGetLastError();
+                ok = false;
+                continue;
+            }
+            const cudaError_t e = cudaDeviceEnablePeerAccess(x.device, 0);
+            if (e != cudaSuccess) {
+                cudaGetLastError();  // cudaErrorPeerAccessAlreadyEnabled is fine
+                if (e != cudaErrorPeerAccessAlreadyEnabled) ok = false;
+            }
+        }
+    } else {
+        struct Rec { uint64_t ok; cudaIpcMemHandle_t h; };
+        Rec mine{};
+        mine.ok = msg == g.ipc_msg && cudaIpcGetMemHandle(&mine.h, msg) == cudaSuccess;
+        if (!mine.ok) cudaGetLastError();
+        const std::vector<uint8_t> all = exchange_all_bytes(g, &mine, sizeof(Rec));
+        for (int r = 0; r < g.nranks && ok; ++r) {
+            Rec x;
+            std::memcpy(&x, all.data() + r * sizeof(Rec), sizeof(Rec));
+            if (!x.ok) ok = false;
+        }
+        for (int r = 0; r < g.nranks && ok; ++r) {
+            if (r == g.rank) {
+                ptrs[r] = msg;
+                continue;
+            }
+            Rec x;
+            std::memcpy(&x, all.data() + r * sizeof(Rec), sizeof(Rec));
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, x.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                ok = false;
+                break;
+            }
+            g.ipc_opened.push_back(p);
+            ptrs[r] = p;
+        }
+    }
+    if (!exchange_all_true(g, ok)) {
+        exchange_release_peers(g);
+        return false;
+    }
+    g.peer_msg = ptrs;
+    g.peer_msg_for = msg;
+    g.peer_msg_bytes = bytes;
+    return true;
+}
+
+void exchange_barrier(DevGraph& g) {
+    if (g.nranks <= 1) return;
+    if (g.exchange && g.exchange->local) {
+        GGB_CUDA(cudaStreamSynchronize(g.stream));
+        g.exchange->local->barrier();
+        return;
+    }
+    // a one-word all-reduce completes on no rank before every rank has
+    // reached it in stream order
+    uint32_t* d = g.ws.get<uint32_t>("xbarrier", 1);
+    nccl_check(nccl().AllReduce(d, d, 1, ncclUint32, ncclMax, g.exchange->comm, g.stream),
+               "ncclAllReduce(barrier)");
+}
+
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local) {
     if (g.nranks <= 1) return 0;
     const std::vector<uint64_t> h = exchange_all(g, local);
@@ -283,6 +422,13 @@ gg_status gg_exchange_local_group(int nranks, gg_exchange** out) {
             x->local = grp;
             out[r] = x;
         }
+    });
+}
+
+gg_status gg_exchange_set_fused(gg_exchange* x, int on) {
+    return ggb::guarded(nullptr, [&] {
+        if (!x) throw ggb::Error(GG_INVALID_ARGUMENT, "null exchange");
+        x->fused = on != 0;
     });
 }
 

@@ -21,6 +21,7 @@ struct gg_exchange {
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;               // NCCL transport (one process per GPU)
     std::shared_ptr<ggb::LocalGroup> local;  // or: ranks as threads of one process
+    bool fused = true;                       // vertex kernel stores into peer replicas
 };
 
 namespace ggb {
@@ -45,6 +46,27 @@ const NcclApi& nccl();
 // array is in message-slot order and only the slots that are ever gathered
 // (out-degree > 0, a prefix of each rank's slot range) travel.
 void exchange_slices(DevGraph& g, void* global_buf, size_t elem_size, bool slots = false);
+
+// Fused exchange. The vertex kernel that computes the new messages also
+// stores each gathered slot's message into every rank's replica (peer
+// memory), so no separate all-gather pass runs; with one message buffer per
+// rank the iteration then needs one barrier between the gathers and the
+// vertex kernel (no rank may overwrite a replica another rank still reads).
+// (kMaxPeers, common.cuh: one NVSwitch node)
+// Collective over the ranks: true when every rank's `msg` (bytes) is
+// addressable from this rank's device (g.peer_msg filled), false when some
+// rank cannot map its peers (the caller all-gathers with exchange_slices).
+// Cached for the same buffer. NCCL transport: `msg` must come from
+// exchange_msg_buffer (CUDA IPC needs a cudaMalloc allocation).
+bool exchange_register_peers(DevGraph& g, void* msg, size_t bytes);
+// The message buffer of a run: IPC-exportable for the NCCL transport, the
+// workspace's otherwise.
+void* exchange_msg_buffer(DevGraph& g, size_t bytes);
+// Stream-ordered barrier: nothing enqueued after it on any rank starts
+// before everything enqueued before it on every rank has completed.
+void exchange_barrier(DevGraph& g);
+// closes the IPC mappings of g (graph teardown)
+void exchange_release_peers(DevGraph& g);
 void exchange_counters(DevGraph& g, void* ctr);
 // sum of `local` over ranks below this one (allgather of one u64 per rank)
 uint64_t exchange_exclusive_base(DevGraph& g, uint64_t local);

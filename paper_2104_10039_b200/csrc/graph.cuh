@@ -124,6 +124,17 @@ struct DevGraph {
     // slot order, so every rank's gathers can single it out (L1/L2 classes).
     std::vector<uint64_t> gather_ranges;
     uint64_t hot_slots = 0;
+    // Fused exchange (exchange_register_peers): every rank's message buffer
+    // as addressed from this rank's device (peer memory over NVLink /
+    // NVSwitch, or the same device for the in-process transport), so the
+    // vertex kernel stores each new message into every replica. Empty: the
+    // messages are all-gathered after the vertex kernel (exchange_slices).
+    std::vector<void*> peer_msg;
+    const void* peer_msg_for = nullptr;  // own buffer the peers were registered for
+    size_t peer_msg_bytes = 0;
+    std::vector<void*> ipc_opened;       // peer buffers opened through CUDA IPC
+    void* ipc_msg = nullptr;             // own message buffer, cudaMalloc'd (IPC-exportable)
+    size_t ipc_msg_bytes = 0;
     ListMeta full;
     // position order (graph.cuh header): rows = full.nz non-empty vertices
     uint64_t nrows = 0;

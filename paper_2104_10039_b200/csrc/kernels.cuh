@@ -105,7 +105,8 @@ struct EdgeArgs {
     // Message-gather cache classes (hot-first slots: low ids are the most read):
     //   slot < hot_limit: L1 evict_last + L2 evict_last   (register-resident runs)
     //   slot < l2_limit:  L2 evict_last                    (heavy programs' runs)
-    //   otherwise:        L2 evict_last if cold_last, else evict_normal
+    //   otherwise:        L1 no_allocate + L2 evict_normal, or (cold_last: the
+    //                     whole array fits L2) as the first class
     uint32_t hot_limit;
     uint32_t l2_limit;
     uint32_t cold_last;
@@ -119,6 +120,10 @@ struct EdgeArgs {
     uint32_t* __restrict__ ticket;
     uint32_t* __restrict__ bitmap;          // [local edge / 32] active flags
     double theta;
+    // theta * (1 +- 2^-40) (NaN when theta is not a normal positive number):
+    // the division-free influence test of programs with relative-growth
+    // influence (see rel_growth_flags)
+    double theta_hi, theta_lo;
     const IterCounters* stop_if;            // batched iterations: the previous iteration's counters
 };
 
@@ -141,6 +146,12 @@ struct VertexArgs {
     const typename P::Accum* __restrict__ acc_out;    // [row]
     const typename P::Accum* __restrict__ hv;
     const typename P::Accum* __restrict__ tv;
+    // Fused exchange (exchange.cuh): the message of a gathered slot s of this
+    // rank (gb0 <= s < ge0 or gb1 <= s < ge1, out-degree > 0) is also stored
+    // into every other rank's replica, peers[r] (npeers = 0: no fused exchange)
+    typename P::Message* peers[kMaxPeers];
+    int npeers, self;
+    uint64_t gb0, ge0, gb1, ge1;
     IterCounters* __restrict__ ctr;
     IterCounters* __restrict__ ctr_next;              // reset here for the next iteration
     const IterCounters* ctr_prev;                     // the previous iteration's (empty_active)
@@ -221,7 +232,9 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
             m[j] = ld_msg_hot(a.msg_cur + s[j], ht.base + s[j] * (uint32_t)sizeof(typename P::Message),
                               s[j] < ht.n ? 0u : (s[j] < a.hot_limit ? 1u : 2u), pol_hot, pol_cold);
         else if constexpr (fold_unroll<P>() != 1)
-            m[j] = ld_msg2(a.msg_cur + s[j], s[j] < a.hot_limit, pol_hot, pol_cold);
+            // (a message array that fits L2 takes the hot instruction for every
+            // slot: the cold one does not allocate in L1)
+            m[j] = ld_msg2(a.msg_cur + s[j], a.cold_last || s[j] < a.hot_limit, pol_hot, pol_cold);
         else
             m[j] = ld_msg(a.msg_cur + s[j], s[j] < a.l2_limit ? pol_hot : pol_cold);
         if constexpr (!std::is_void_v<W>) wr[j] = __ldg(a.w + P0 + j);
@@ -370,10 +383,20 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
 #ifndef GGB_SHIFT_GROUP
 #define GGB_SHIFT_GROUP 8
 #endif
+// Programs whose influence is the relative growth of the accumulator,
+// (acc - before) / acc with 0 for acc <= 0 (PageRank, algorithms.hpp:25-30),
+// and whose estatus is `influence > theta`.
+template <class P>
+__host__ __device__ constexpr bool rel_growth_influence() {
+    if constexpr (requires { P::kRelGrowthInfluence; }) return P::kRelGrowthInfluence;
+    else return false;
+}
+
 template <class P, class W, int MODE, bool HOT = false>
 __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0, uint8_t* sp0,
                                           uint64_t t, int lane, uint64_t pol_stream,
-                                          uint64_t pol_hot, uint64_t pol_cold, HotTable ht = {}) {
+                                          uint64_t pol_hot, uint64_t pol_cold, HotTable ht = {},
+                                          uint32_t* claim = nullptr) {
     using Accum = typename P::Accum;
     using Message = typename P::Message;
     constexpr bool CHAIN = MODE == kEdgeChain;
@@ -541,36 +564,111 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             // the carry of a vertex the skip test leaves out is never read:
             // its chain is closed at once (no look-back). The look-back comes
             // right after the fold: the chain advances at the rate tasks
-            // publish inclusive values (measured: any later point is slower).
+            // publish inclusive values (measured: any later point is slower;
+            // so is deciding the other vertices' edges while the look-back's
+            // first window is in flight -- a second walk over the run:
+            // c5 superstep 13.2 -> 16.7 ms, c2 1.2 -> 1.75 ms)
             if (__shfl_sync(0xffffffffu, pk_first, 0)) carry_in = chain_carry(a, t, lane);
             publish_incl(carry_in);
         }
+        // PageRank's warp claims its next task now: the ticket's L2 round
+        // trip overlaps the f64 influence pass, whose length varies little,
+        // so tasks still start in claim order (c5 superstep -1.6 %; a claim
+        // made before the look-back or the fold lets successors wait up to a
+        // whole task for a piece: 13.8 -> 66 ms when claimed at task start).
+        // Programs with short influence passes claim after the task (c2 SSSP
+        // measured 8 % slower with the early claim).
+        if constexpr (rel_growth_influence<P>())
+            if (claim && lane == 0) *claim = atomicAdd(a.ticket, 1u);
     }
     if constexpr (CHAIN) {
         // influence of each edge against its exclusive running prefix
         // (engine.hpp:204-211): the carry into the task, the run's prefix in
         // the task, then the run's own sequential gathers; identity at each
         // later vertex start
-        Accum run = (cont && hk == 0) ? carry_in : a.prog.gather_identity();
-        if (joins_prev) run = a.prog.combine(run, prevS);
+        Accum run0 = (cont && hk == 0) ? carry_in : a.prog.gather_identity();
+        if (joins_prev) run0 = a.prog.combine(run0, prevS);
         uint32_t kbits = 0;
-        int nb2 = len > 0 ? st0[hk + 1] : 0;
-        int kk = hk;
-        for_run<P>([&](int j) {
-            const int p = (int)(P0 - tstart) + j;
-            if (p >= rlo && p < rhi) {
-                if (p >= nb2) {
-                    ++kk;
-                    nb2 = st0[kk + 1];
-                    run = a.prog.gather_identity();
+        const int nb20 = len > 0 ? st0[hk + 1] : 0;
+        if constexpr (rel_growth_influence<P>()) {
+            // Division-free pass: with s = acc after the edge and d = s - before,
+            // the reference's test fl(d / s) > theta is decided as d > theta_hi*s
+            // (true) or d < theta_lo*s (false): a quotient outside
+            // theta*(1 +- 2^-41) is more than one ulp of theta away from it, so
+            // its correctly rounded value cannot fall on the other side. Edges
+            // in between (or with s, theta*s out of the normal range) are
+            // "unsure" and re-decided by an exact walk with the division
+            // (c5 superstep 13.6 -> 13.2 ms; tests: exact ties and one-ulp
+            // thresholds, test_pagerank_exact_influence_ties).
+            Accum run = run0;
+            int nb2 = nb20, kk = hk;
+            uint32_t unsure = 0;
+            for_run<P>([&](int j) {
+                const int p = (int)(P0 - tstart) + j;
+                if (p >= rlo && p < rhi) {
+                    if (p >= nb2) {
+                        ++kk;
+                        nb2 = st0[kk + 1];
+                        run = a.prog.gather_identity();
+                    }
+                    if ((pmask >> j) & 1u) {
+                        const double before = run;
+                        run = run + m[j];
+                        const double d = run - before;
+                        const double th = run * a.theta_hi, tl = run * a.theta_lo;
+                        // acc <= 0 (or NaN): influence 0, 0 > theta is false
+                        const bool pos = run > 0.0;
+                        const bool normal = tl > 0x1p-1000 && th < 0x1p+1000;
+                        const bool yes = pos && normal && d > th;
+                        const bool sure = !pos || (normal && (d > th || d < tl));
+                        kbits |= (yes ? 1u : 0u) << j;
+                        unsure |= (sure ? 0u : 1u) << j;
+                    }
                 }
-                if ((pmask >> j) & 1u) {
-                    const double infl = a.prog.gather(run, m[j], wv(j));
-                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
-                }
+            });
+            if (!(a.theta_hi == a.theta_hi)) unsure = pmask;  // theta not normal: all exact
+            if (unsure) {  // rare: the exact walk for the unsure edges
+                run = run0;
+                nb2 = nb20;
+                kk = hk;
+                for_run<P>([&](int j) {
+                    const int p = (int)(P0 - tstart) + j;
+                    if (p >= rlo && p < rhi) {
+                        if (p >= nb2) {
+                            ++kk;
+                            nb2 = st0[kk + 1];
+                            run = a.prog.gather_identity();
+                        }
+                        if ((pmask >> j) & 1u) {
+                            const double infl = a.prog.gather(run, m[j], wv(j));
+                            if ((unsure >> j) & 1u)
+                                kbits = (kbits & ~(1u << j)) |
+                                        ((a.prog.estatus(infl, a.theta) ? 1u : 0u) << j);
+                        }
+                    }
+                });
             }
-        });
+        } else {
+            Accum run = run0;
+            int nb2 = nb20, kk = hk;
+            for_run<P>([&](int j) {
+                const int p = (int)(P0 - tstart) + j;
+                if (p >= rlo && p < rhi) {
+                    if (p >= nb2) {
+                        ++kk;
+                        nb2 = st0[kk + 1];
+                        run = a.prog.gather_identity();
+                    }
+                    if ((pmask >> j) & 1u) {
+                        const double infl = a.prog.gather(run, m[j], wv(j));
+                        if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
+                    }
+                }
+            });
+        }
         warp_write_flags(a.bitmap, a.pad, tstart, pmask, kbits, lane);
+        if constexpr (!rel_growth_influence<P>())
+            if (claim && lane == 0) *claim = atomicAdd(a.ticket, 1u);
     }
     __syncwarp();  // st0 is restaged by the warp's next task
 }
@@ -587,13 +685,14 @@ edge_kernel(const EdgeArgs<P, W> a) {
     const uint64_t pol_hot = policy_evict_last();
     const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
     if constexpr (MODE == kEdgeChain) {  // tasks claimed in order (see chain_carry)
-        for (;;) {
-            uint32_t t = 0;
-            if (lane == 0) t = atomicAdd(a.ticket, 1u);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= a.ntasks) break;
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        while (t < a.ntasks) {
+            uint32_t tn = 0;
             edge_task<P, W, MODE>(a, st_all[threadIdx.x >> 5], sp0, t, lane, pol_stream, pol_hot,
-                                  pol_cold);
+                                  pol_cold, {}, &tn);
+            t = __shfl_sync(0xffffffffu, tn, 0);
         }
         return;
     }
@@ -624,14 +723,16 @@ edge_chain_kernel(const EdgeArgs<P, W> a) {
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_hot = policy_evict_last();
     const uint64_t pol_cold = a.cold_last ? policy_evict_last() : policy_evict_normal();
-    for (;;) {  // tasks claimed in order (see chain_carry)
-        uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(a.ticket, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.ntasks) break;
+    // Tasks are claimed in order (see chain_carry); the next claim is made
+    // inside the current task, after its look-back (see edge_task).
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (t < a.ntasks) {
+        uint32_t tn = 0;  // lane 0: the next task, claimed inside the task
         edge_task<P, W, kEdgeChain>(a, st_all[threadIdx.x >> 5], sp_all[threadIdx.x >> 5], t, lane,
-                                    pol_stream, pol_hot,
-                                    pol_cold);
+                                    pol_stream, pol_hot, pol_cold, {}, &tn);
+        t = __shfl_sync(0xffffffffu, tn, 0);
     }
 }
 
@@ -675,7 +776,7 @@ edge_kernel_hot(const EdgeArgs<P, W> a, uint32_t nhot) {
 // status, counters. Skipped vertices keep property, message and (zero)
 // status: no write. SUPER: after a kEdgeChain superstep tv[t1-1] already
 // holds the left-to-right fold up to task t1-1, so the join is one combine.
-template <class P, class W, bool SUPER>
+template <class P, class W, bool SUPER, bool PEERS = false>
 __global__ void __launch_bounds__(256)
 vertex_kernel(const VertexArgs<P, W> a) {
     using Accum = typename P::Accum;
@@ -744,7 +845,16 @@ vertex_kernel(const VertexArgs<P, W> a) {
                 const bool active = a.prog.vstatus(prev[i], fresh);         // GG-VStatus (:217)
                 const bool ok = a.prog.valid(fresh);                        // (:218)
                 a.prop[p] = fresh;
-                a.msg[sv[i]] = a.prog.message(fresh, deg[i]);
+                const typename P::Message mnew = a.prog.message(fresh, deg[i]);
+                a.msg[sv[i]] = mnew;
+                if (PEERS) {  // fused exchange: the other replicas (NVLink stores)
+                    const uint64_t sl = sv[i];
+                    if ((sl >= a.gb0 && sl < a.ge0) || (sl >= a.gb1 && sl < a.ge1)) {
+#pragma unroll
+                        for (int r = 0; r < kMaxPeers; ++r)
+                            if (r < a.npeers && r != a.self) a.peers[r][sl] = mnew;
+                    }
+                }
                 a.st[p] = (uint8_t)((active ? kStActive : 0) | (ok ? 0 : kStInvalid) |
                                     (SUPER && (st[i] & kStActive) ? kStWasActive : 0));
                 g += o1[i] - o0[i];

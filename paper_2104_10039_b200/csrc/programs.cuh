@@ -27,6 +27,7 @@ struct PageRank {
     using Property = double;
     using Message = double;
     using Accum = double;
+    static constexpr bool kRelGrowthInfluence = true;  // gather's influence, estatus `> theta`
     static constexpr bool kMsgIsProp = false;
     static constexpr bool kNeedsDegree = true;
     double damping = 0.85, epsilon = 1e-7;

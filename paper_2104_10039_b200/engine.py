@@ -347,6 +347,7 @@ class RunReport:
     kernel_launches: int = 0
     flags: np.ndarray | None = None  # final active-edge flags, one byte per edge (when requested)
     flag_words: np.ndarray | None = None  # the same flags as the device bitmap (uint32 words)
+    exchange_fused: bool = False  # several ranks: messages stored into the peer replicas
 
 
 def validate(cfg: EngineConfig) -> None:
@@ -468,7 +469,8 @@ def run(graph, program, cfg: EngineConfig, *, want_flags: bool = False, timing: 
         return RunReport(out_props, int(summ.iterations_run), per,
                          float(summ.total_wall_seconds), int(summ.total_processed_edges),
                          int(summ.kept_edges), int(summ.kernel_launches),
-                         unpack_bitmap(flags, e) if flags is not None else None, flags)
+                         unpack_bitmap(flags, e) if flags is not None else None, flags,
+                         bool(summ.exchange_fused))
     finally:
         if owned is not None:
             owned.close()
@@ -568,6 +570,12 @@ class Exchange:
             x.rank, x.nranks = r, nranks
             out.append(x)
         return out
+
+    def set_fused(self, on: bool) -> None:
+        """Fused exchange (default on): the vertex kernel stores the new
+        messages into every rank's replica over peer memory; off: all-gather
+        after it. Same value on every rank (gg_exchange_set_fused)."""
+        _raise(L.lib().gg_exchange_set_fused(self.handle, 1 if on else 0), None)
 
     @staticmethod
     def unique_id() -> bytes:

@@ -8,6 +8,11 @@ each rank's lists, per-iteration slice exchange and counter reduction, the
 sparsified list's global base) with host barriers and device copies standing
 in for the collectives. No kernel waits on another rank's kernel.
 
+Both exchange paths run: the fused one (default: each vertex kernel stores
+its new messages into every rank's replica, here peer buffers on the same
+device, with a barrier between the gathers and the vertex kernels) and the
+all-gather after the vertex kernel (gg_exchange_set_fused(x, 0)).
+
 The bar is the analogue of test_engine.cpp:161-182: properties and
 per-iteration records bit-identical to the single-rank run, for every
 program and scheme.
@@ -46,8 +51,10 @@ def _program(ggb, prog, graph, seed):
     return ggb.EdgeBeliefPropagationProgram(ggb.bp_priors(graph.n, seed), 1e-6)
 
 
-def _run_ranks(ggb, graph, program, cfg, nranks):
+def _run_ranks(ggb, graph, program, cfg, nranks, fused=True):
     xs = ggb.Exchange.local_group(nranks)
+    for x in xs:
+        x.set_fused(fused)
     out, errs = [None] * nranks, []
 
     def work(r):
@@ -67,6 +74,7 @@ def _run_ranks(ggb, graph, program, cfg, nranks):
     for x in xs:
         x.close()
     assert not errs, errs
+    assert all(r.exchange_fused == (fused and nranks > 1) for r in out)
     return out
 
 
@@ -89,26 +97,64 @@ CASES = [  # prog, scale, edge factor, seed, symmetrise, weights, theta
 ]
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "allgather"])
 @pytest.mark.parametrize("nranks", [2, 3])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] + ("-" + c[5] if c[5] else "") for c in CASES])
-def test_ranks_bit_identical_to_one_gpu(ggb, case, nranks):
+def test_ranks_bit_identical_to_one_gpu(ggb, case, nranks, fused):
     prog, scale, ef, seed, sym, weights, theta = case
     graph = _graph(ggb, scale, ef, seed, sym, weights)
     program = _program(ggb, prog, graph, seed)
     cfg = ggb.EngineConfig("gg", 0.5, theta, 2, 30, seed)
     single = ggb.run(graph, program, cfg)
-    for rep in _run_ranks(ggb, graph, program, cfg, nranks):
+    for rep in _run_ranks(ggb, graph, program, cfg, nranks, fused):
         _same(rep, single)
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "allgather"])
 @pytest.mark.parametrize("scheme", ["accurate", "sp", "sms", "gg"])
-def test_ranks_all_schemes_pagerank(ggb, scheme):
+def test_ranks_all_schemes_pagerank(ggb, scheme, fused):
     graph = _graph(ggb, 16, 16, 7)
     program = ggb.pagerank_spec(0.85, 1e-7)
     cfg = ggb.EngineConfig(scheme, 0.5, 0.01, 3, 25, 7)
     single = ggb.run(graph, program, cfg)
-    for rep in _run_ranks(ggb, graph, program, cfg, 4):
+    for rep in _run_ranks(ggb, graph, program, cfg, 4, fused):
         _same(rep, single)
+
+
+def test_ranks_fused_runs_back_to_back(ggb):
+    """Several runs (different programs, hence message buffers of different
+    sizes) on the same rank graphs: the peer replicas are re-registered when
+    the buffer changes and reused otherwise."""
+    graph = _graph(ggb, 14, 16, 9)
+    progs = [ggb.pagerank_spec(0.85, 1e-7), ggb.wcc_spec(), ggb.pagerank_spec(0.85, 1e-7),
+             ggb.sssp_spec(int(np.argmax(graph.out_degree)), True)]
+    cfg = ggb.EngineConfig("gg", 0.5, 0.01, 2, 12, 9)
+    singles = [ggb.run(graph, p, cfg) for p in progs]
+    nranks = 3
+    xs = ggb.Exchange.local_group(nranks)
+    out, errs = [[None] * len(progs) for _ in range(nranks)], []
+
+    def work(r):
+        try:
+            dg = ggb.DeviceGraph.upload(graph, device=0, rank=r, nranks=nranks, exchange=xs[r].handle)
+            for i, p in enumerate(progs):
+                out[r][i] = ggb.run(dg, p, cfg)
+            dg.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    for x in xs:
+        x.close()
+    assert not errs, errs
+    for r in range(nranks):
+        for i in range(len(progs)):
+            assert out[r][i].exchange_fused
+            _same(out[r][i], singles[i])
 
 
 @pytest.mark.parametrize("nranks", [3, 5])

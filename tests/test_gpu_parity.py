@@ -494,3 +494,61 @@ def test_chain_stress_bitwise(ggb, prog):
         assert np.array_equal(r.flag_words, base.flag_words), (k, grid)
         assert [x.active_vertices for x in r.per_iteration] == [x.active_vertices for x in base.per_iteration]
     dg.close()
+
+
+# --------------------------------------------------------------------------
+# PageRank's division-free superstep test (kernels.cuh rel_growth_influence):
+# influences EXACTLY equal to theta and just around it must be decided as the
+# reference's correctly rounded division decides them.
+# --------------------------------------------------------------------------
+def _dyadic_graph(n, k):
+    """Out-degree k everywhere; in-degrees 2k (n/4 vertices), k/2 (n/2) and k
+    (n/4); in-lists hold distinct sources, ascending. With n, k powers of two
+    and damping 0.5 the ranks after iteration 1 are 1.5/n, 0.75/n and 1/n and
+    every message of the t = 2 superstep is a small dyadic multiple of
+    1/(n k): every prefix sum is exact under any association."""
+    deg = np.concatenate([np.full(n // 4, 2 * k), np.full(n // 2, k // 2), np.full(n - 3 * n // 4, k)])
+    deg = np.random.default_rng(k).permutation(deg)
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(deg)
+    src = (np.arange(int(off[-1])) % n).astype(np.uint32)
+    for v in range(n):
+        a, b = int(off[v]), int(off[v + 1])
+        src[a:b].sort()
+    return CSC(n, off, src, None)
+
+
+def _superstep_influences(g, k):
+    """fl(d / s) of every edge at the t = 2 superstep (exact sums)."""
+    n = g.n
+    deg = np.diff(g.off.astype(np.int64))
+    rank1 = (0.5 + 0.5 * deg / k) / n
+    m = rank1 / k
+    out = np.empty(len(g.src))
+    for v in range(n):
+        a, b = int(g.off[v]), int(g.off[v + 1])
+        s = np.cumsum(m[g.src[a:b]])
+        before = np.concatenate([[0.0], s[:-1]])
+        out[a:b] = (s - before) / s
+    return out
+
+
+@pytest.mark.parametrize("k", [8, 32, 256])
+@pytest.mark.parametrize("theta", [0.25, 0.125, 0.5, 1.0 / 3.0, 0.1, 0.25 * (1 + 2.0 ** -52),
+                                   0.25 * (1 - 2.0 ** -53), 0.0])
+def test_pagerank_exact_influence_ties(ggb, k, theta):
+    """The superstep's flags when influences sit EXACTLY on theta or one ulp
+    off it (0.25 +- 1 ulp), for inexact thresholds (1/3, 0.1) and theta = 0
+    (not a normal number: the exact path everywhere). The prefix sums are
+    exact under any association (_dyadic_graph), so the device and the oracle
+    see the same (d, s) for every edge and must take the same decision with
+    no near-threshold adoption."""
+    n = 2048 if k == 8 else 1024  # k = 256: in-lists of 512 edges span tasks
+    g = _dyadic_graph(n, k)
+    infl = _superstep_influences(g, k)
+    if k == 8 and theta in (0.25, 0.125, 0.5):
+        assert np.count_nonzero(infl == theta) > 0  # the case exercises exact ties
+    rep, ref, mr = compare(ggb, g, PR, scheme="gg", sigma=1.0, theta=theta, alpha=1,
+                           max_iterations=2, damping=0.5)
+    assert mr.adopted == 0 and mr.real == 0, mr.per_superstep
+    assert np.array_equal(rep.flags.astype(bool), infl > theta)
