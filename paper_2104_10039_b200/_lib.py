@@ -101,7 +101,8 @@ def lib():
             f"libggb.so not found at {LIB_PATH}: run __graft_entry__.build() (no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     missing = [s for s in EXPORTS if not hasattr(L, s)]
-    if missing:
+    # an A/B library (GGB_LIB_PATH, tools/ab.py) may predate newer entry points
+    if missing and not os.environ.get("GGB_LIB_PATH"):
         raise ImportError(f"libggb.so lacks symbols {missing}")
     L.gg_abi_version.restype = C.c_int
     if L.gg_abi_version() != ABI_VERSION:
@@ -147,14 +148,15 @@ def lib():
     L.gg_nccl_unique_id.argtypes = [vp]
     L.gg_exchange_nccl_create.argtypes = [vp, C.c_int, C.c_int, P(vp), P(ErrorC)]
     L.gg_exchange_destroy.argtypes = [vp]
-    L.gg_exchange_set_fused.argtypes = [vp, C.c_int]
+    if hasattr(L, "gg_exchange_set_fused"):
+        L.gg_exchange_set_fused.argtypes = [vp, C.c_int]
     L.gg_exchange_local_group.argtypes = [C.c_int, P(vp)]
     L.gg_topk_error.argtypes = [vp, vp, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.gg_relative_error.argtypes = [vp, vp, C.c_uint64, P(C.c_double)]
     L.gg_stretch_error.argtypes = [vp, vp, C.c_uint64, P(C.c_double)]
     for s in EXPORTS:
         if s not in ("gg_status_string", "gg_mode_for", "gg_select_superstep_iterations",
-                     "gg_abi_version"):
+                     "gg_abi_version") and s not in missing:
             getattr(L, s).restype = C.c_int
     _lib = L
     return L

@@ -13,6 +13,7 @@
 #include "exchange.cuh"
 #include <cmath>
 #include <cstdlib>
+#include <vector>
 #include <type_traits>
 
 #include "graph.cuh"
@@ -487,12 +488,17 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
 }
 
 // Sparsified-list layout in one pass over the owned vertices (replaces
-// soff + nonempty flag / scan / fill of build_runs): s_off[v] = rank of
-// off[v] among the kept edges; the non-empty vertices get consecutive nz
-// indices (decoupled look-back over tiles of kLayoutTile vertices; warp w
-// owns the tile's vertices [128w, 128w + 128), lane l vertices 32j + l) with
-// nz_vid / nz_start and the run marks of nonempty_fill_kernel; the thread
-// holding v = nloc writes the sentinels nz_start[nz] and run_i[nruns] = nz - 1.
+// soff + nonempty flag / scan / fill of build_runs and the run-map max-scan):
+// s_off[v] = rank of off[v] among the kept edges; the non-empty vertices get
+// consecutive nz indices (decoupled look-back over tiles of kLayoutTile
+// vertices; warp w owns the tile's vertices [128w, 128w + 128), lane l
+// vertices 32j + l) with nz_vid / nz_start, and every run r whose first
+// padded position lies in non-empty vertex i's positions [s, e) gets
+// run_i[r] = i, i.e. runs [ceil(s/16), ceil(e/16)) (the first non-empty
+// vertex also takes the runs before it); a vertex of more than 32 runs is
+// written by its whole warp. The thread holding v = nloc writes the
+// sentinels nz_start[nz] and run_i[r] = nz - 1 for the runs after the last
+// kept edge, run_i[nruns] included.
 constexpr int kLayoutVPT = 8;  // vertices per thread (c5: 8 -> 0.75 ms, 4 -> 0.89, 2 -> 1.20, 16 -> 0.75)
 constexpr int kLayoutTile = 256 * kLayoutVPT;
 
@@ -501,7 +507,7 @@ sp_layout_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
                  const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ wpref,
                  uint64_t pad, uint64_t nruns, uint64_t* __restrict__ s_off,
                  uint32_t* __restrict__ nz_vid, uint64_t* __restrict__ nz_start,
-                 uint32_t* __restrict__ marks, uint32_t* __restrict__ run_i,
+                 uint32_t* __restrict__ run_i,
                  unsigned long long* __restrict__ tstate, uint32_t* __restrict__ ticket,
                  uint64_t ntiles) {
     __shared__ uint32_t s_tile;
@@ -522,13 +528,18 @@ sp_layout_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
         }
         const uint64_t vend = vb + 32 * kLayoutVPT;  // lane 31's last successor
         const uint64_t so_end = (lane == 31 && vend <= nloc) ? bit_rank(bitmap, wpref, __ldg(off + vend)) : 0ull;
+        // kept offset of vertex (vb + 32j + lane) + 1
+        auto next_of = [&](int j) -> uint64_t {
+            uint64_t nx = __shfl_down_sync(0xffffffffu, so[j], 1);
+            const uint64_t nx0 = __shfl_sync(0xffffffffu, j + 1 < kLayoutVPT ? so[j + 1 < kLayoutVPT ? j + 1 : j] : so_end, 0);
+            if (lane == 31) nx = j + 1 < kLayoutVPT ? nx0 : so_end;
+            return nx;
+        };
         uint32_t fl = 0, off_in[kLayoutVPT], run = 0;
 #pragma unroll
         for (int j = 0; j < kLayoutVPT; ++j) {
             const uint64_t v = vb + 32 * j + lane;
-            uint64_t nx = __shfl_down_sync(0xffffffffu, so[j], 1);
-            const uint64_t nx0 = __shfl_sync(0xffffffffu, j + 1 < kLayoutVPT ? so[j + 1 < kLayoutVPT ? j + 1 : j] : so_end, 0);
-            if (lane == 31) nx = j + 1 < kLayoutVPT ? nx0 : so_end;
+            const uint64_t nx = next_of(j);  // warp-collective: every lane, no short-circuit
             const bool f = v < nloc && nx > so[j];
             fl |= (f ? 1u : 0u) << j;
             const uint32_t b = __ballot_sync(0xffffffffu, f);
@@ -551,21 +562,39 @@ sp_layout_kernel(const uint64_t* __restrict__ off, uint64_t nloc,
         }
         __syncthreads();
         const uint64_t wbase = s_wbase[warp];
+        auto run_ceil = [&](uint64_t kept_off) { return (kept_off + pad + kRun - 1) / kRun; };
 #pragma unroll
-        for (int j = 0; j < kLayoutVPT; ++j) {
+        for (int j = 0; j < kLayoutVPT; ++j) {  // every lane runs every j (warp-wide writes below)
             const uint64_t v = vb + 32 * j + lane;
-            if (v > nloc) break;
-            s_off[v] = so[j];
+            const uint64_t nx = next_of(j);
             const uint64_t i = wbase + off_in[j];
+            uint64_t r_lo = 0, r_hi = 0;  // runs of this lane's vertex
+            uint32_t val = 0;
+            if (v <= nloc) s_off[v] = so[j];
             if (v == nloc) {  // sentinels: i = nz
                 nz_start[i] = so[j];
-                run_i[nruns] = i ? (uint32_t)(i - 1) : 0u;
-            } else if ((fl >> j) & 1u) {
+                r_lo = i ? run_ceil(so[j]) : 0;
+                r_hi = nruns + 1;
+                val = i ? (uint32_t)(i - 1) : 0u;
+            } else if (v < nloc && ((fl >> j) & 1u)) {
                 nz_vid[i] = (uint32_t)v;
                 nz_start[i] = so[j];
-                const uint64_t sp = so[j] + pad;
-                const uint64_t r = sp <= pad ? 0 : (sp + kRun - 1) / kRun;
-                if (r < nruns) atomicMax(marks + r, (uint32_t)i);
+                r_lo = i ? run_ceil(so[j]) : 0;
+                r_hi = run_ceil(nx);
+                if (r_hi > nruns) r_hi = nruns;
+                val = (uint32_t)i;
+            }
+            const bool longv = r_hi > r_lo + 32;
+            if (!longv)
+                for (uint64_t r = r_lo; r < r_hi; ++r) run_i[r] = val;
+            uint32_t lb = __ballot_sync(0xffffffffu, longv);
+            while (lb) {  // long vertices: the warp writes their runs together
+                const int src = __ffs(lb) - 1;
+                lb &= lb - 1;
+                const uint64_t a0 = __shfl_sync(0xffffffffu, r_lo, src);
+                const uint64_t a1 = __shfl_sync(0xffffffffu, r_hi, src);
+                const uint32_t x = __shfl_sync(0xffffffffu, val, src);
+                for (uint64_t r = a0 + lane; r < a1; r += 32) run_i[r] = x;
             }
         }
         __syncthreads();  // s_tile / s_wsum / s_wbase reuse
@@ -585,9 +614,7 @@ static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint6
     meta.nz = 0;  // on the device only
     meta.nz_vid = g.ws.get<uint32_t>("sp.nz_vid", g.nrows + 1);
     meta.nz_start = g.ws.get<uint64_t>("sp.nz_start", g.nrows + 1);
-    uint32_t* marks = g.ws.get<uint32_t>("sp.runmark", meta.nruns + 1);
     meta.run_i = g.ws.get<uint32_t>("sp.run_i", meta.nruns + 1);
-    if (meta.nruns) GGB_CUDA(cudaMemsetAsync(marks, 0, meta.nruns * 4, g.stream));
     const uint64_t ntiles = (g.nrows + 1 + kLayoutTile - 1) / kLayoutTile;
     auto* tstate = g.ws.get<unsigned long long>("sp.tstate", ntiles + 1);
     auto* ticket = reinterpret_cast<uint32_t*>(tstate + ntiles);
@@ -595,16 +622,9 @@ static void build_sparse_layout(DevGraph& g, const uint32_t* bitmap, const uint6
     static const int per_sm = occupancy_grid((const void*)sp_layout_kernel, 256, 0, 1);
     const uint64_t gr = std::min<uint64_t>(ntiles, (uint64_t)per_sm * g.num_sms);
     sp_layout_kernel<<<gr, 256, 0, g.stream>>>(g.full.nz_start, g.nrows, bitmap, wpref, pad, meta.nruns,
-                                               s_off, meta.nz_vid, meta.nz_start, marks, meta.run_i,
+                                               s_off, meta.nz_vid, meta.nz_start, meta.run_i,
                                                tstate, ticket, ntiles);
     GGB_CUDA(cudaGetLastError());
-    if (!meta.nruns) return;
-    size_t tmp = 0;
-    GGB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp, marks, meta.run_i, MaxU32{}, meta.nruns,
-                                            g.stream));
-    void* tmpp = g.ws.get("cub.tmp.sp.runs", tmp);
-    GGB_CUDA(cub::DeviceScan::InclusiveScan(tmpp, tmp, marks, meta.run_i, MaxU32{}, meta.nruns,
-                                            g.stream));
 }
 
 // Initial sparsification overlapped with the graph upload

@@ -170,3 +170,38 @@ def test_ranks_with_tiny_and_empty_slices(ggb, nranks):
         single = ggb.run(graph, prog, cfg)
         for rep in _run_ranks(ggb, graph, prog, cfg, nranks):
             _same(rep, single)
+
+
+def test_ranks_agree_on_the_exchange_path(ggb):
+    """Ranks asking for different exchange paths (rank 0 fused, the others
+    not) agree on the all-gather through the registration's agreement round:
+    no rank stores into replicas another rank does not expect."""
+    graph = _graph(ggb, 14, 16, 10)
+    program = ggb.pagerank_spec(0.85, 1e-7)
+    cfg = ggb.EngineConfig("gg", 0.5, 0.01, 2, 12, 10)
+    single = ggb.run(graph, program, cfg)
+    nranks = 3
+    xs = ggb.Exchange.local_group(nranks)
+    for r, x in enumerate(xs):
+        x.set_fused(r == 0)
+    out, errs = [None] * nranks, []
+
+    def work(r):
+        try:
+            dg = ggb.DeviceGraph.upload(graph, device=0, rank=r, nranks=nranks, exchange=xs[r].handle)
+            out[r] = ggb.run(dg, program, cfg)
+            dg.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    for x in xs:
+        x.close()
+    assert not errs, errs
+    for rep in out:
+        assert not rep.exchange_fused
+        _same(rep, single)
