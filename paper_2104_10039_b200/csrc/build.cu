@@ -86,6 +86,13 @@ __device__ __forceinline__ uint32_t sparsify_word(uint64_t i, uint64_t e_loc, ui
         const uint64_t k0 = key ^ (e_base + e0);
         const uint32_t Thi = (uint32_t)(T >> 32);
         uint32_t tie = 0;
+        if ((uint32_t)T == 0) {
+            // T's low word is 0 (sigma a multiple of 2^-32, e.g. 0.5): a high-word
+            // tie means h >= T, so the high-word test alone decides
+#pragma unroll 8
+            for (int b = 0; b < 32; ++b) word |= (mix_hi(k0 ^ (uint64_t)b) < Thi ? 1u : 0u) << b;
+            return word;
+        }
 #pragma unroll 8
         for (int b = 0; b < 32; ++b) {
             const uint32_t h = mix_hi(k0 ^ (uint64_t)b);
@@ -676,7 +683,7 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
         GGB_CUDA(cudaStreamSynchronize(g.stream));
         build_sparse_layout(g, bitmap, wpref, s_off, 0, kept, meta);
         if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-        if (launches) *launches += 3;
+        if (launches) *launches += 2;  // scan_compact, sp_layout
         return kept;
     }
     // several ranks: the list's padded base needs the kept counts of all
@@ -704,7 +711,7 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
     }
     build_sparse_layout(g, bitmap, wpref, s_off, pad, kept, meta);
     if (ev1) GGB_CUDA(cudaEventRecord(ev1, g.stream));
-    if (launches) *launches += 3;
+    if (launches) *launches += 2;  // compact, sp_layout
     return kept;
 }
 

@@ -248,7 +248,7 @@ struct Engine {
             s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
             if (g.pre_sparse && g.pre_sigma == cfg.sigma && g.pre_seed == cfg.seed) {
                 kept = presparse_finish(g, s_off, sp);  // sparsified during the upload
-                launches += 2;
+                launches += 1;  // sp_layout
             } else {
                 const SparsifySpec hs = sparsify_spec(cfg.sigma, cfg.seed, false);
                 kept = rebuild_sparse(g, bitmap, s_off, s_src, s_w, sp, nullptr, nullptr, &launches,

@@ -407,6 +407,9 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
     const uint64_t hi = P0 + kRun < a.e_end ? P0 + kRun : a.e_end;
     // non-empty vertices touching the task: [i0, i_next], starts staged
     const uint32_t i0 = a.run_i[t * kWarp];
+    // the next task's first run (run_i[nruns] = nz - 1 is the sentinel): loaded
+    // before the gathers' inline asm, which the compiler may not move loads across
+    const uint32_t i_next = a.run_i[(t + 1) * kWarp];
     Message m[kRun];
     WStore<W> wr[kRun];
     int len = 0;
@@ -423,8 +426,6 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
-    const uint64_t rn = (t + 1) * kWarp;
-    const uint32_t i_next = a.run_i[rn];  // run_i[nruns] = nz - 1 (sentinel)
     const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
     for (uint32_t j = lane; j < cnt; j += kWarp) {
         const int64_t rel = (int64_t)(a.nz_start[i0 + j] + a.pad) - (int64_t)tstart;
