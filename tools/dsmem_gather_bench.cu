@@ -1,0 +1,219 @@
+// dsmem_gather_bench.cu — calibration microbenchmark (not part of the product):
+// can a thread-block cluster's distributed shared memory serve the hottest
+// message slots at a rate that ADDS to the LDG path (bound by ~1 L1TEX tag
+// lookup per cycle per SM for random 8-byte gathers)?
+//
+//   ./dsmem_gather_bench <mode> <cluster> <log2 slots per CTA> [reps] [threads]
+//     mode: ldg   every gather through ld.global.nc (the baseline)
+//           dsm   slots < cluster * T from the cluster's tables
+//                 (ld.shared::cluster, slot s lives in CTA s % cluster),
+//                 the rest through ld.global.nc
+//           lds   slots < T from the CTA's own table, the rest ld.global.nc
+//           skip  slots < cluster * T not gathered at all (the bound)
+//
+// Index stream: the hot-first slot marginal of an R-MAT s26 source (same
+// emulation as tma_gather_bench.cu). Messages: f64[2^26].
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+namespace cg = cooperative_groups;
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            std::printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                    \
+            std::exit(1);                                                             \
+        }                                                                             \
+    } while (0)
+
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__global__ void make_idx(uint32_t* idx, uint64_t m) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        for (int l = 0; l < 26; ++l)
+            k += (double)(mix64(i * 64 + l + 99) >> 11) * 0x1.0p-53 < 0.24 ? 1 : 0;
+        double c = 1.0, cum = 0.0;  // C(26, j)
+        for (int j = 0; j < k; ++j) { cum += c; c = c * (26 - j) / (j + 1); }
+        const double u2 = (double)(mix64(i * 64 + 63) >> 11) * 0x1.0p-53;
+        idx[i] = (uint32_t)(cum + floor(u2 * c));
+    }
+}
+
+__global__ void fill(double* x, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] = (double)(i & 1023) * 0.5;
+}
+
+__global__ void count_hot(const uint32_t* idx, uint64_t m, uint32_t h, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        c += idx[i] < h;
+    atomicAdd(out, c);
+}
+
+enum { kLdg = 0, kDsm = 1, kLds = 2, kSkip = 3 };
+
+template <int MODE>
+__global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double* __restrict__ x,
+                      int tlog, int clog, double* __restrict__ out) {
+    extern __shared__ __align__(16) double tab[];
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t rank = MODE == kDsm ? cl.block_rank() : 0;
+    const uint32_t T = 1u << tlog, C = 1u << clog;
+    uint32_t base0 = 0, stride = 0;
+    if (MODE == kDsm || MODE == kLds) {
+        // dsm: slot s lives in CTA s % C at row s / C; lds: the first T slots
+        for (uint32_t i = threadIdx.x; i < T; i += blockDim.x)
+            tab[i] = MODE == kDsm ? x[(uint64_t)i * C + rank] : x[i];
+        const uint32_t la = (uint32_t)__cvta_generic_to_shared(tab);
+        base0 = la;
+        if (MODE == kDsm) {
+            uint32_t a0, a1;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a0) : "r"(la), "r"(0));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a1) : "r"(la), "r"(C > 1 ? 1 : 0));
+            base0 = a0;
+            stride = a1 - a0;
+            cl.sync();
+        } else {
+            __syncthreads();
+        }
+    }
+    const uint32_t H = MODE == kLdg ? 0 : MODE == kLds ? T : T * C;
+    const int lane = threadIdx.x & 31;
+    const uint64_t wpb = blockDim.x >> 5;
+    const uint64_t gw = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (uint64_t)gridDim.x * wpb;
+    double acc = 0.0;
+    for (uint64_t c = gw; c < m / 512; c += nw) {
+        uint32_t s[16];
+        const uint4* ip = reinterpret_cast<const uint4*>(idx + c * 512) + lane * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint4 v = __ldg(ip + q);
+            s[4 * q] = v.x; s[4 * q + 1] = v.y; s[4 * q + 2] = v.z; s[4 * q + 3] = v.w;
+        }
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const double* gp = x + s[j];
+            if (MODE == kLdg) {
+                asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v[j]) : "l"(gp));
+            } else if (MODE == kSkip) {
+                v[j] = 0.0;
+                asm volatile("{.reg .pred p; setp.ge.u32 p, %1, %2; @p ld.global.nc.f64 %0, [%3];}"
+                             : "+d"(v[j]) : "r"(s[j]), "r"(H), "l"(gp));
+            } else if (MODE == kLds) {
+                const uint32_t sa = base0 + s[j] * 8;
+                asm volatile(
+                    "{.reg .pred p; setp.lt.u32 p, %1, %2; @p ld.shared.f64 %0, [%3];"
+                    " @!p ld.global.nc.f64 %0, [%4];}"
+                    : "=d"(v[j]) : "r"(s[j]), "r"(H), "r"(sa), "l"(gp));
+            } else {
+                const uint32_t sa = base0 + (s[j] & (C - 1)) * stride + (s[j] >> clog) * 8;
+                asm volatile(
+                    "{.reg .pred p; setp.lt.u32 p, %1, %2; @p ld.shared::cluster.f64 %0, [%3];"
+                    " @!p ld.global.nc.f64 %0, [%4];}"
+                    : "=d"(v[j]) : "r"(s[j]), "r"(H), "r"(sa), "l"(gp));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc += v[j];
+    }
+    if (MODE == kDsm) cl.sync();  // peers may still be reading this CTA's table
+    if (acc == 1.2345) out[0] = acc;
+}
+
+template <int MODE>
+static void run(const char* name, int clog, int tlog, int reps, int threads, const uint32_t* idx, uint64_t m,
+                const double* x, double* out, unsigned long long* cnt) {
+    const int C = 1 << clog;
+    const size_t smem = (MODE == kDsm || MODE == kLds) ? (size_t)8 << tlog : 0;
+    auto k = bench<MODE>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (MODE == kDsm && C > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = MODE == kDsm ? C : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int grid;
+    if (MODE == kDsm) {
+        cfg.gridDim = dim3(C * 64);
+        int ncl = 0;
+        CK(cudaOccupancyMaxActiveClusters(&ncl, k, &cfg));
+        grid = ncl * C;
+    } else {
+        int per = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, threads, smem));
+        grid = per * sms;
+    }
+    cfg.gridDim = dim3(grid);
+    const uint32_t H = MODE == kLdg ? 0 : MODE == kLds ? (1u << tlog) : (uint32_t)C << tlog;
+    CK(cudaMemset(cnt, 0, 8));
+    count_hot<<<1024, 256>>>(idx, m, H, cnt);
+    unsigned long long hc = 0;
+    CK(cudaMemcpy(&hc, cnt, 8, cudaMemcpyDeviceToHost));
+    CK(cudaLaunchKernelEx(&cfg, k, idx, m, x, tlog, clog, out));
+    CK(cudaDeviceSynchronize());
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int i = 0; i < reps; ++i) CK(cudaLaunchKernelEx(&cfg, k, idx, m, x, tlog, clog, out));
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= reps;
+    std::printf("mode=%s cluster=%d slots/CTA=2^%d threads=%d grid=%d hot=%.1f%%: %.3f ms, %.1f G gathers/s\n",
+                name, C, tlog, threads, grid, 100.0 * (double)hc / (double)m, ms,
+                (double)m / (ms * 1e-3) / 1e9);
+}
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "ldg";
+    const int C = argc > 2 ? std::atoi(argv[2]) : 8;
+    const int tlog = argc > 3 ? std::atoi(argv[3]) : 13;
+    const int reps = argc > 4 ? std::atoi(argv[4]) : 5;
+    const int threads = argc > 5 ? std::atoi(argv[5]) : 512;
+    int clog = 0;
+    while ((1 << clog) < C) ++clog;
+    const uint64_t n = 1ull << 26, m = 1ull << 28;
+    double *x, *out;
+    uint32_t* idx;
+    unsigned long long* cnt;
+    CK(cudaMalloc(&x, n * 8));
+    CK(cudaMalloc(&idx, m * 4));
+    CK(cudaMalloc(&out, 8));
+    CK(cudaMalloc(&cnt, 8));
+    fill<<<4096, 256>>>(x, n);
+    make_idx<<<4096, 256>>>(idx, m);
+    CK(cudaDeviceSynchronize());
+    if (mode == "ldg") run<kLdg>("ldg", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "dsm") run<kDsm>("dsm", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "lds") run<kLds>("lds", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else run<kSkip>("skip", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    return 0;
+}
