@@ -66,6 +66,25 @@ __device__ __forceinline__ uint32_t mix_hi(uint64_t x) {
     const uint32_t xhi = __umulhi(ylo, c_lo) + ylo * c_hi + yhi * c_lo;
     return xhi ^ (xhi >> 31);
 }
+constexpr uint64_t kMixC1 = 0xbf58476d1ce4e5b9ull;
+// mix_hi from mix64's first product P on: high word of the final mix.
+__device__ __forceinline__ uint32_t mix_hi_tail(uint64_t P) {
+    const uint64_t y = P ^ (P >> 27);
+    const uint32_t ylo = (uint32_t)y, yhi = (uint32_t)(y >> 32);
+    constexpr uint32_t c_lo = 0x133111ebu, c_hi = 0x94d049bbu;  // 0x94d049bb133111eb
+    const uint32_t xhi = __umulhi(ylo, c_lo) + ylo * c_hi + yhi * c_lo;
+    return xhi ^ (xhi >> 31);
+}
+// Bit i of the result = bit (i ^ k) of w, k < 32 (five conditional swaps of
+// adjacent 2^j-bit groups).
+__device__ __forceinline__ uint32_t xor_permute_bits(uint32_t w, uint32_t k) {
+    if (k & 1u) w = ((w & 0x55555555u) << 1) | ((w >> 1) & 0x55555555u);
+    if (k & 2u) w = ((w & 0x33333333u) << 2) | ((w >> 2) & 0x33333333u);
+    if (k & 4u) w = ((w & 0x0f0f0f0fu) << 4) | ((w >> 4) & 0x0f0f0f0fu);
+    if (k & 8u) w = ((w & 0x00ff00ffu) << 8) | ((w >> 8) & 0x00ff00ffu);
+    if (k & 16u) w = (w << 16) | (w >> 16);
+    return w;
+}
 __device__ __forceinline__ bool keep_edge(uint64_t x, uint64_t T) {
     const uint32_t hhi = mix_hi(x), Thi = (uint32_t)(T >> 32);
     if (hhi != Thi) return hhi < Thi;
@@ -82,24 +101,47 @@ __device__ __forceinline__ uint32_t sparsify_word(uint64_t i, uint64_t e_loc, ui
     uint32_t word = 0;
     if (keep_all) {
         word = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
-    } else if (nb == 32 && (e_base & 31) == 0) {  // key ^ (base | b) = (key ^ base) ^ b
+    } else if (nb == 32 && (e_base & 31) == 0) {
+        // The 32 hashed values k0 ^ b are the aligned block U0 + c, c = kc ^ b
+        // (kc = k0 & 31). After mix64's first step they are A0 + 21 + c
+        // (A0 = U0 + (golden & ~31), 32-aligned): c <= 10 falls in block A0
+        // at offset r = c + 21, c >= 11 in block A0 + 32 at r = c - 11. Inside
+        // a block A the shifted term S = (A | r) >> 30 = A >> 30 is constant,
+        // so x ^ (x >> 30) = ((A ^ S) & ~31) + (r ^ (S & 31)) and the first
+        // product is P0 + (r ^ m) * C1 with P0 = ((A ^ S) & ~31) * C1, m =
+        // S & 31: two multiply-adds per edge instead of the add, the
+        // xor-shift and the 64-bit product (all mod 2^64, so block A0 + 32
+        // wrapping or crossing a 2^30 boundary needs no special case).
+        // Flags are collected at bit c and moved to bit b = c ^ kc at the end.
         const uint64_t k0 = key ^ (e_base + e0);
+        const uint32_t kc = (uint32_t)k0 & 31u;
+        const uint64_t A0 = (k0 & ~31ull) + (0x9e3779b97f4a7c15ull & ~31ull);
+        const uint64_t Qa = A0 ^ (A0 >> 30), A1 = A0 + 32, Qb = A1 ^ (A1 >> 30);
+        const uint64_t Pa = (Qa & ~31ull) * kMixC1, Pb = (Qb & ~31ull) * kMixC1;
+        const uint32_t ma = (uint32_t)Qa & 31u, mb = (uint32_t)Qb & 31u;
         const uint32_t Thi = (uint32_t)(T >> 32);
-        uint32_t tie = 0;
-        if ((uint32_t)T == 0) {
-            // T's low word is 0 (sigma a multiple of 2^-32, e.g. 0.5): a high-word
-            // tie means h >= T, so the high-word test alone decides
-#pragma unroll 8
-            for (int b = 0; b < 32; ++b) word |= (mix_hi(k0 ^ (uint64_t)b) < Thi ? 1u : 0u) << b;
-            return word;
+        uint32_t wp = 0, tp = 0;
+        auto hash_c = [&](int c) {  // c is a compile-time constant after unrolling
+            const uint32_t rp = (uint32_t)((c + 21) & 31) ^ (c >= 11 ? mb : ma);
+            return mix_hi_tail((c >= 11 ? Pb : Pa) + (uint64_t)rp * kMixC1);
+        };
+        // T's low word 0 (sigma a multiple of 2^-32, e.g. 0.5): a high-word tie
+        // means h >= T, so the high-word test alone decides
+        const bool ties = (uint32_t)T != 0;
+        if (!ties) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) wp |= (hash_c(c) < Thi ? 1u : 0u) << c;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const uint32_t h = hash_c(c);
+                wp |= (h < Thi ? 1u : 0u) << c;
+                tp |= (h == Thi ? 1u : 0u) << c;
+            }
         }
-#pragma unroll 8
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t h = mix_hi(k0 ^ (uint64_t)b);
-            word |= (h < Thi ? 1u : 0u) << b;
-            tie |= (h == Thi ? 1u : 0u) << b;
-        }
-        while (tie) {
+        word = xor_permute_bits(wp, kc);
+        uint32_t tie = ties ? xor_permute_bits(tp, kc) : 0u;
+        while (tie) {  // probability ~2^-32 per edge
             const int b = __ffs(tie) - 1;
             tie &= tie - 1;
             if (mix64(k0 ^ (uint64_t)b) < T) word |= 1u << b;
@@ -387,13 +429,25 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
         }
         uint32_t word[kScanWPL], off[kScanWPL];  // off: exclusive popcount within the warp
         uint32_t run = 0;
+        if constexpr (HASH) {
+            // one copy of the 32 unrolled hashes (rolled over the lane's words:
+            // four inlined copies overflow the instruction cache)
+#pragma unroll 1
+            for (int j = 0; j < kScanWPL; ++j) {
+                const uint64_t wi = w0 + 32 * j + lane;
+                uint32_t x = 0;
+                if (wi < nwords) x = sparsify_word(wi, e_loc, e_base, h.T, h.key, h.keep_all);
+                if (wi <= nwords) bitmap[wi] = x;  // [nwords]: zero guard word
+#pragma unroll
+                for (int q = 0; q < kScanWPL; ++q) word[q] = q == j ? x : word[q];
+            }
+        }
 #pragma unroll
         for (int j = 0; j < kScanWPL; ++j) {
             const uint64_t wi = w0 + 32 * j + lane;
             uint32_t x = 0;
             if constexpr (HASH) {
-                if (wi < nwords) x = sparsify_word(wi, e_loc, e_base, h.T, h.key, h.keep_all);
-                if (wi <= nwords) bitmap[wi] = x;  // [nwords]: zero guard word
+                x = word[j];
             } else {
                 if (wi < nwords) x = __ldg(bitmap + wi);
             }

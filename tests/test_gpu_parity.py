@@ -354,6 +354,13 @@ def test_device_sparsify_matches_reference_hash(ggb):  # engine.cpp:63-75, test_
     assert int(ggb.sparsify(e, 1.0, 9).sum()) == e and int(ggb.sparsify(e, 0.0, 9).sum()) == 0
     lo, hi = ggb.sparsify(2000, 0.3, 5), ggb.sparsify(2000, 0.7, 5)
     assert np.all(hi[lo == 1] == 1)
+    # thresholds with a non-zero low word (high-word ties resolved exactly), every
+    # key & 31 class of the word-block decomposition, a ragged last word
+    for sigma, seed in [(0.3, 5), (0.7, 6), (0.05, 11), (0.999, 2), (1e-7, 4), (1 / 3, 123456789)]:
+        e = 1_000_003 + seed % 29
+        assert np.array_equal(ggb.sparsify(e, sigma, seed), Oracle.sparsify(e, sigma, seed)), (sigma, seed)
+    for seed in range(40, 72):
+        assert np.array_equal(ggb.sparsify(4099, 0.4, seed), Oracle.sparsify(4099, 0.4, seed)), seed
 
 
 # --------------------------------------------------------------------------

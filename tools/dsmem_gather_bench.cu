@@ -67,7 +67,7 @@ __global__ void count_hot(const uint32_t* idx, uint64_t m, uint32_t h, unsigned 
     atomicAdd(out, c);
 }
 
-enum { kLdg = 0, kDsm = 1, kLds = 2, kSkip = 3 };
+enum { kLdg = 0, kDsm = 1, kLds = 2, kSkip = 3, kPol2 = 4, kPol1 = 5, kWin = 6 };
 
 template <int MODE>
 __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double* __restrict__ x,
@@ -95,6 +95,11 @@ __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double
         }
     }
     const uint32_t H = MODE == kLdg ? 0 : MODE == kLds ? T : T * C;
+    const uint32_t hot_limit = 3u << 20;  // 24 MB of f64 slots, as the engine's c5 classes
+    uint64_t pol_stream, pol_hot, pol_cold;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hot));
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_cold));
     const int lane = threadIdx.x & 31;
     const uint64_t wpb = blockDim.x >> 5;
     const uint64_t gw = (uint64_t)blockIdx.x * wpb + (threadIdx.x >> 5), nw = (uint64_t)gridDim.x * wpb;
@@ -104,15 +109,28 @@ __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double
         const uint4* ip = reinterpret_cast<const uint4*>(idx + c * 512) + lane * 4;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint4 v = __ldg(ip + q);
+            uint4 v;
+            if (MODE >= kPol2)
+                asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ip + q), "l"(pol_stream));
+            else
+                v = __ldg(ip + q);
             s[4 * q] = v.x; s[4 * q + 1] = v.y; s[4 * q + 2] = v.z; s[4 * q + 3] = v.w;
         }
         double v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const double* gp = x + s[j];
-            if (MODE == kLdg) {
+            if (MODE == kLdg || MODE == kWin) {
                 asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v[j]) : "l"(gp));
+            } else if (MODE == kPol1) {
+                asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v[j]) : "l"(gp), "l"(pol_hot));
+            } else if (MODE == kPol2) {
+                asm volatile(
+                    "{.reg .pred p; setp.lt.u32 p, %1, %2;"
+                    " @p ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%3], %4;"
+                    " @!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%3], %5;}"
+                    : "=d"(v[j]) : "r"(s[j]), "r"(hot_limit), "l"(gp), "l"(pol_hot), "l"(pol_cold));
             } else if (MODE == kSkip) {
                 v[j] = 0.0;
                 asm volatile("{.reg .pred p; setp.ge.u32 p, %1, %2; @p ld.global.nc.f64 %0, [%3];}"
@@ -151,13 +169,25 @@ static void run(const char* name, int clog, int tlog, int reps, int threads, con
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = MODE == kDsm ? C : 1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (MODE == kWin) {
+        // tlog here = log2 of the window's MB
+        const size_t wbytes = (size_t)1 << (20 + tlog - 10) ;  // tlog 14 -> 16 MB, 15 -> 32 MB
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes));
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow.base_ptr = (void*)x;
+        at[1].val.accessPolicyWindow.num_bytes = wbytes;
+        at[1].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+        cfg.numAttrs = 2;
+    }
     int grid;
     if (MODE == kDsm) {
         cfg.gridDim = dim3(C * 64);
@@ -214,6 +244,9 @@ int main(int argc, char** argv) {
     if (mode == "ldg") run<kLdg>("ldg", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else if (mode == "dsm") run<kDsm>("dsm", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else if (mode == "lds") run<kLds>("lds", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "pol2") run<kPol2>("pol2", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "pol1") run<kPol1>("pol1", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "win") run<kWin>("win", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else run<kSkip>("skip", clog, tlog, reps, threads, idx, m, x, out, cnt);
     return 0;
 }
