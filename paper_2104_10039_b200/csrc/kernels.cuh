@@ -667,6 +667,21 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 }
             });
         }
+        // The next task (claimed above; its ticket has arrived by now): pull its
+        // sources and run map into L2 while this task writes its flags, so the
+        // task starts with L2 hits (c5 superstep 13.26 -> 12.92 ms; also
+        // prefetching its vertices' starts and skip-test inputs needs the run
+        // map's value first and measured slower, 13.14 ms)
+        if constexpr (rel_growth_influence<P>()) {
+            if (claim) {
+                const uint32_t tn = __shfl_sync(0xffffffffu, *claim, 0);
+                if (tn < a.ntasks && lane <= 16) {
+                    const void* pf = lane < 16 ? (const void*)(a.src + (uint64_t)tn * kChunkEdges + lane * 32)
+                                               : (const void*)(a.run_i + (uint64_t)tn * kWarp);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+                }
+            }
+        }
         warp_write_flags(a.bitmap, a.pad, tstart, pmask, kbits, lane);
         if constexpr (!rel_growth_influence<P>())
             if (claim && lane == 0) *claim = atomicAdd(a.ticket, 1u);
