@@ -51,6 +51,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GTEPS of full and sparsified gather iterations; % of HBM roofline"
+GATHER_PEAK_G = 264.3  # G random 8-byte gathers/s, one B200 (profiles/r2_dsmem_gather_bench.txt)
 WORKLOADS = {
     "c1": dict(prog="pr", scale=16, ef=16, seed=1, theta=0.01, weights=None, sym=False),
     "c2": dict(prog="sssp", scale=22, ef=16, seed=2, theta=0.05, weights="u32", sym=False),
@@ -262,6 +263,21 @@ def summarize(args, wl, reps, info, e, per_rank_frac, peak_info):
         if gbs(per, "vertex_bytes", "vertex_ms") else None,
         "full_gather_edge_gbs": round(gbs(full), 1) if gbs(full) else None,
     }
+    # The gather's second ceiling: every random message gather is one L1TEX
+    # tag lookup, ~0.9 per clock per SM on B200 whatever cache level serves it
+    # (tools/dsmem_gather_bench.cu, `ldg` rows of profiles/r2_dsmem_gather_bench.txt;
+    # shared-memory, DSMEM and TMA gather4 paths do not add to it, r2_summary.md).
+    t_dom = sum(i.edge_ms for i in dom)
+    if t_dom:
+        ach = sum(i.processed_edges for i in dom) * per_rank_frac / (t_dom / 1e3) / 1e9
+        roofline["gather_request_bound"] = {
+            "unit": "G gathers/s", "achieved": round(ach, 1), "peak": GATHER_PEAK_G,
+            "frac": round(ach / GATHER_PEAK_G, 4),
+            "peak_source": "measured pure LDG gather rate on the hot-first R-MAT s26 slot stream "
+                           "(profiles/r2_dsmem_gather_bench.txt, 256-thread CTAs)",
+            "hbm_frac_at_peak": round(GATHER_PEAK_G * (sum(i.edge_bytes for i in dom) /
+                                      max(sum(i.processed_edges for i in dom) * per_rank_frac, 1)) / peak, 4)
+            if peak else None}
     return roofline, gteps(approx), gteps(full), per
 
 
