@@ -7,7 +7,6 @@
 cd $GRAFT_REPO_ROOT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/f_smi.txt 2>&1
 timeout 300 python -m pytest tests -m gpu -q -p no:cacheprovider --ignore=tests/test_gpu_full_size.py -rf -x > gpurun_out/f_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/f_pytest.log
-timeout 300 python tools/ab.py c5 LIB=abl/head.so:head base:prod --rounds 2 > gpurun_out/f_ab_c5.jsonl 2>&1
 timeout 420 python bench.py --steps 10 --warmup 3 > gpurun_out/f_bench_c5.json 2> gpurun_out/f_bench_c5.err
 for w in c1 c2 c3 c4; do
   timeout 200 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/f_bench_$w.json 2> gpurun_out/f_bench_$w.err
@@ -32,3 +31,5 @@ if [ -f /tmp/f_c5.ncu-rep ]; then
   gzip -c /tmp/f_chain_src.csv > gpurun_out/f_c5_chain_source.csv.gz
   du -sh gpurun_out >> gpurun_out/f_ncu_full.log
 fi
+timeout 400 python bench.py --workload c5 --gpus 4 --transport local --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_bench_c5_local4.json 2> gpurun_out/f_bench_c5_local4.err
+timeout 300 python bench.py --workload c4 --gpus 2 --transport local --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/f_bench_c4_local2.json 2> gpurun_out/f_bench_c4_local2.err
