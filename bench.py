@@ -268,7 +268,9 @@ def summarize(args, wl, reps, info, e, per_rank_frac, peak_info):
     # (tools/dsmem_gather_bench.cu, `ldg` rows of profiles/r2_dsmem_gather_bench.txt;
     # shared-memory, DSMEM and TMA gather4 paths do not add to it, r2_summary.md).
     t_dom = sum(i.edge_ms for i in dom)
-    if t_dom:
+    # (PageRank only: 8-byte messages gathered with plain loads; the 4-byte
+    # programs also serve hot slots from shared memory, BP's gather is ALU-heavy)
+    if t_dom and wl["prog"] == "pr":
         ach = sum(i.processed_edges for i in dom) * per_rank_frac / (t_dom / 1e3) / 1e9
         roofline["gather_request_bound"] = {
             "unit": "G gathers/s", "achieved": round(ach, 1), "peak": GATHER_PEAK_G,
