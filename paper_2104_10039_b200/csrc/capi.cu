@@ -662,4 +662,12 @@ gg_status gg_stretch_error(const double* approx, const double* exact, uint64_t n
     });
 }
 
+#ifdef GGB_CHAIN_STATS
+// diagnostic build only: look-back statistics of the chain kernels since the last call
+void ggb_debug_chain_stats(unsigned long long* out) {
+    unsigned long long z[8] = {};
+    cudaMemcpyFromSymbol(out, ggb::g_chain_stats, sizeof(z));
+    cudaMemcpyToSymbol(ggb::g_chain_stats, z, sizeof(z));
+}
+#endif
 }  // extern "C"

@@ -321,6 +321,9 @@ __device__ __forceinline__ uint32_t chain_get(const ulonglong2* d, Accum& v) {
     return same ? (uint32_t)st[0] : 0u;
 }
 
+#ifdef GGB_CHAIN_STATS
+__device__ unsigned long long g_chain_stats[8];
+#endif
 template <class P, class W>
 __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a, uint64_t t, int lane) {
     using Accum = typename P::Accum;
@@ -328,6 +331,9 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
     int64_t base = (int64_t)t - 1;  // newest task of the window; lane i looks at base - i
     Accum v = a.prog.gather_identity();
     int L;
+#ifdef GGB_CHAIN_STATS
+    unsigned sleeps = 0, adv = 0;
+#endif
     for (;;) {
         const int64_t j = base - lane;
         uint32_t s = kChainIncl;
@@ -342,10 +348,28 @@ __device__ __forceinline__ typename P::Accum chain_carry(const EdgeArgs<P, W>& a
             if ((none & ((1u << L) - 1u)) == 0) break;
         } else if (!none) {
             base -= kWarp;  // 32 pieces, no inclusive value yet: look further back
+#ifdef GGB_CHAIN_STATS
+            ++adv;
+#endif
             continue;
         }
+#ifdef GGB_CHAIN_STATS
+        ++sleeps;
+#endif
         __nanosleep(64);  // a piece in between is still being folded
     }
+#ifdef GGB_CHAIN_STATS
+    if (lane == 0) {
+        atomicAdd(&g_chain_stats[0], 1ull);
+        atomicAdd(&g_chain_stats[1], (unsigned long long)sleeps);
+        atomicAdd(&g_chain_stats[2], (unsigned long long)adv);
+        if (sleeps == 0) atomicAdd(&g_chain_stats[3], 1ull);
+        if (sleeps > 8) atomicAdd(&g_chain_stats[4], 1ull);
+        if (sleeps > 64) atomicAdd(&g_chain_stats[5], 1ull);
+        if (adv > 4) atomicAdd(&g_chain_stats[6], 1ull);
+        atomicMax(&g_chain_stats[7], (unsigned long long)(sleeps + adv));
+    }
+#endif
     if constexpr (!kPacked) {  // values from L2 after the acquire
         __syncwarp();
         const int64_t j = base - lane;
