@@ -212,6 +212,19 @@ def load_traffic(workload):
         return None, None
 
 
+def load_mask_parity(workload):
+    """Active-edge mask parity of this workload at full size against the lock-step
+    oracle: the record written by tests/test_gpu_full_size.py (GGB_PARITY_OUT) on
+    a B200 and committed as profiles/mask_parity.json. North-star: masks identical
+    except edges whose influence lies within rounding of theta, their count reported."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "mask_parity.json")))[workload]
+    except Exception:
+        return None
+    return d | {"source": "profiles/mask_parity.json (tests/test_gpu_full_size.py, lock-step oracle, "
+                          "every flag after every superstep)"}
+
+
 def device_accuracy(ggb, wl, n, acc_proj, dg, rep, acc_edges):
     """Score of the gg run against the accurate run on the device (the
     reference sweep's metric per algorithm, bench.cpp:181-190 / :280-287);
@@ -458,6 +471,7 @@ def ours(args):
         "gteps_sparsified_kernel": round(g_sp, 3) if g_sp else None,
         "gteps_full_kernel": round(g_full, 3) if g_full else None,
         "accuracy": accuracy,
+        "mask_parity": load_mask_parity(args.workload),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clk,
         # per iteration of one run: processed edges / vertices (engine.hpp:186-189,

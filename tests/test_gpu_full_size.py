@@ -82,6 +82,17 @@ def _full(ggb, name):
           f"{int(orc.flags.sum())} active flags; supersteps {orc.lockstep}; "
           f"near-threshold edges in the band {near}, decided differently {adopted}, "
           f"real mismatches {real}, final mask mismatches {mism}")
+    out_dir = os.environ.get("GGB_PARITY_OUT")  # the one-off record bench.py reports (profiles/mask_parity.json)
+    if out_dir:
+        import json
+        with open(os.path.join(out_dir, f"mask_parity_{name}.json"), "w") as f:
+            json.dump({"workload": name, "program": wl["prog"], "edges": int(g.e),
+                       "iterations": int(rep.iterations_run), "supersteps": len(orc.lockstep),
+                       "flags_compared_per_superstep": int(g.e),
+                       "near_threshold_edges_in_band": int(near),
+                       "near_threshold_edges_decided_differently": int(adopted),
+                       "real_mismatches": int(real), "final_mask_mismatches": mism,
+                       "band_unit": NEAR_UNIT[prog]}, f)
     assert all(s["compared"] for s in orc.lockstep)
     assert real == 0
     assert mism == 0
