@@ -108,14 +108,35 @@ def config_json(args, wl, world, transport="nccl"):
 # clocks during the timed region
 # --------------------------------------------------------------------------
 class ClockSampler:
+    """`nvidia-smi -lms 50` beside the run. It is started BEFORE the warm-up (its
+    start-up, tens of ms of driver queries, used to land inside the first timed
+    step and stretch a host sync there by several ms); only the samples whose
+    timestamps fall inside the timed region [begin(), end()] are reported."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+              "clocks_event_reasons.sw_power_cap,utilization.gpu,timestamp")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
+
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+
+    def _in_window(self, stamp):
+        if self.t0 is None or self.t1 is None:
+            return True
+        try:
+            import datetime
+            t = datetime.datetime.strptime(stamp, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except Exception:
+            return True
+        return self.t0 - 0.05 <= t <= self.t1 + 0.05
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -137,11 +158,15 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         rows = []
+        every = []
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                rows.append(parts)
+                every.append(parts)
         os.unlink(self.path)
+        rows = [r for r in every if len(r) < 8 or self._in_window(r[7])]
+        if not rows and every:  # region shorter than the sampling period: the nearest sample
+            rows = every[-1:]
         if not rows:  # region shorter than the sampling period: one immediate sample
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -344,6 +369,8 @@ def ours(args):
     n, e = dg.n, dg.e
     info = dg.info()
     program = make_program(ggb, wl, dg, n)
+    clocks = ClockSampler(local)
+    clocks.start()  # before the accurate run and the warm-up: see ClockSampler
     acc = ggb.run(dg, program, ggb.EngineConfig("accurate", max_iterations=budget_for(wl, n)),
                   device_output=True)
     acc_proj = ggb.DeviceBuffer.copy(dg.last_projection())
@@ -360,14 +387,14 @@ def ours(args):
 
     for _ in range(args.warmup):
         ggb.run(dg, program, cfg, device_output=True)
-    clocks = ClockSampler(local)
     barrier()
-    clocks.start()
+    clocks.begin()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     reps = [ggb.run(dg, program, cfg, timing=True, device_output=True) for _ in range(args.steps)]
     ev1.record()
     barrier()
+    clocks.end()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
     if dist:
