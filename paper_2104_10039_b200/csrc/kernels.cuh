@@ -484,6 +484,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         if (len > 0) pk = sp0[k];
     const bool pk_first = pk;  // lane 0: the task's first vertex
     uint32_t pmask = 0;  // edges of processed vertices (flags we own)
+    uint32_t bmask = 0;  // run positions at which a new vertex starts
     Accum x = a.prog.gather_identity(), hvv = x;
     bool head_closed = false;
     auto fold_step = [&](int j, const Message& mj, double wj) {
@@ -500,6 +501,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                 ++k;
                 nb = st0[k + 1];
                 if constexpr (MODE != kEdgePlain) pk = sp0[k];
+                if constexpr (CHAIN) bmask |= 1u << j;
             }
             if (pk) {
                 (void)a.prog.gather(x, mj, wj);
@@ -614,7 +616,6 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         Accum run0 = (cont && hk == 0) ? carry_in : a.prog.gather_identity();
         if (joins_prev) run0 = a.prog.combine(run0, prevS);
         uint32_t kbits = 0;
-        const int nb20 = len > 0 ? st0[hk + 1] : 0;
         if constexpr (rel_growth_influence<P>()) {
             // Division-free pass: with s = acc after the edge and d = s - before,
             // the reference's test fl(d / s) > theta is decided as d > theta_hi*s
@@ -625,17 +626,14 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             // "unsure" and re-decided by an exact walk with the division
             // (c5 superstep 13.6 -> 13.2 ms; tests: exact ties and one-ulp
             // thresholds, test_pagerank_exact_influence_ties).
+            // (vertex starts and the run's valid range come from the fold:
+            // bmask marks the positions where it moved to the next vertex,
+            // pmask holds only in-range positions of processed vertices)
             Accum run = run0;
-            int nb2 = nb20, kk = hk;
             uint32_t unsure = 0;
             for_run<P>([&](int j) {
-                const int p = (int)(P0 - tstart) + j;
-                if (p >= rlo && p < rhi) {
-                    if (p >= nb2) {
-                        ++kk;
-                        nb2 = st0[kk + 1];
-                        run = a.prog.gather_identity();
-                    }
+                {
+                    if ((bmask >> j) & 1u) run = a.prog.gather_identity();
                     if ((pmask >> j) & 1u) {
                         const double before = run;
                         run = run + m[j];
@@ -654,8 +652,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             if (!(a.theta_hi == a.theta_hi)) unsure = pmask;  // theta not normal: all exact
             if (unsure) {  // rare: the exact walk for the unsure edges
                 run = run0;
-                nb2 = nb20;
-                kk = hk;
+                int nb2 = len > 0 ? st0[hk + 1] : 0, kk = hk;
                 for_run<P>([&](int j) {
                     const int p = (int)(P0 - tstart) + j;
                     if (p >= rlo && p < rhi) {
@@ -675,19 +672,11 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
             }
         } else {
             Accum run = run0;
-            int nb2 = nb20, kk = hk;
             for_run<P>([&](int j) {
-                const int p = (int)(P0 - tstart) + j;
-                if (p >= rlo && p < rhi) {
-                    if (p >= nb2) {
-                        ++kk;
-                        nb2 = st0[kk + 1];
-                        run = a.prog.gather_identity();
-                    }
-                    if ((pmask >> j) & 1u) {
-                        const double infl = a.prog.gather(run, m[j], wv(j));
-                        if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
-                    }
+                if ((bmask >> j) & 1u) run = a.prog.gather_identity();
+                if ((pmask >> j) & 1u) {
+                    const double infl = a.prog.gather(run, m[j], wv(j));
+                    if (a.prog.estatus(infl, a.theta)) kbits |= 1u << j;
                 }
             });
         }
