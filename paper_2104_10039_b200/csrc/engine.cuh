@@ -336,6 +336,20 @@ struct Engine {
                 const bool normal = cfg.theta > 0x1p-900 && cfg.theta < 0x1p+900;
                 ea.theta_hi = normal ? cfg.theta * (1.0 + 0x1p-40) : std::nan("");
                 ea.theta_lo = normal ? cfg.theta * (1.0 - 0x1p-40) : std::nan("");
+                // accumulators whose products with theta_hi/lo stay inside
+                // [2^-998, 2^998]: binary exponents [lo_e, hi_e]
+                ea.pn_lo = ea.pn_span = 0;
+                if (normal) {
+                    int et = 0;
+                    (void)std::frexp(cfg.theta, &et);  // theta = f * 2^et, f in [0.5, 1)
+                    int lo_e = -998 - (et - 1) + 1, hi_e = 998 - et - 1;
+                    lo_e = std::max(lo_e, -1022);
+                    hi_e = std::min(hi_e, 1023);
+                    if (lo_e <= hi_e) {
+                        ea.pn_lo = (uint32_t)(lo_e + 1023) << 20;
+                        ea.pn_span = (uint32_t)(hi_e - lo_e + 1) << 20;
+                    }
+                }
             }
             ea.stop_if = k ? ring + (u - 1) % kRing : nullptr;
             VertexArgs<P, W> va{};

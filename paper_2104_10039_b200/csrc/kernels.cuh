@@ -124,6 +124,10 @@ struct EdgeArgs {
     // the division-free influence test of programs with relative-growth
     // influence (see rel_growth_flags)
     double theta_hi, theta_lo;
+    // run > 0, finite, and run * theta_hi/lo inside [2^-998, 2^998], as one
+    // unsigned test on the accumulator's high word: (hi32(run) - pn_lo) < pn_span
+    // (pn_span = 0: never, every edge takes the exact walk)
+    uint32_t pn_lo, pn_span;
     const IterCounters* stop_if;            // batched iterations: the previous iteration's counters
 };
 
@@ -639,17 +643,17 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
                         run = run + m[j];
                         const double d = run - before;
                         const double th = run * a.theta_hi, tl = run * a.theta_lo;
-                        // acc <= 0 (or NaN): influence 0, 0 > theta is false
-                        const bool pos = run > 0.0;
-                        const bool normal = tl > 0x1p-1000 && th < 0x1p+1000;
-                        const bool yes = pos && normal && d > th;
-                        const bool sure = !pos || (normal && (d > th || d < tl));
-                        kbits |= (yes ? 1u : 0u) << j;
-                        unsure |= (sure ? 0u : 1u) << j;
+                        // positive, finite, products in the normal range: one
+                        // integer test on the high word; anything else (acc <= 0,
+                        // NaN, extreme magnitudes) goes to the exact walk
+                        const bool pn = (uint32_t)__double2hiint(run) - a.pn_lo < a.pn_span;
+                        const bool hi_side = d > th;
+                        kbits |= ((pn && hi_side) ? 1u : 0u) << j;
+                        unsure |= ((pn && (hi_side || d < tl)) ? 0u : 1u) << j;
                     }
                 }
             });
-            if (!(a.theta_hi == a.theta_hi)) unsure = pmask;  // theta not normal: all exact
+            // (theta not a normal number: pn_span = 0, every edge is unsure)
             if (unsure) {  // rare: the exact walk for the unsure edges
                 run = run0;
                 int nb2 = len > 0 ? st0[hk + 1] : 0, kk = hk;
