@@ -361,6 +361,7 @@ def ours(args):
         dist.broadcast_object_list(uid, src=0)
         exchange = ggb.Exchange(rank, world, uid[0])
         exchange.set_fused(not args.no_fused)
+        exchange.selftest()  # ragged all-gather + all-reduces against closed forms, before any work
     wl = WORKLOADS[args.workload]
     t_setup = time.perf_counter()
     dg = ggb.DeviceGraph.rmat(wl["scale"], wl["ef"], wl["seed"], symmetrize=wl["sym"],

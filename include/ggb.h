@@ -246,6 +246,13 @@ gg_status gg_exchange_local_group(int nranks, gg_exchange** out);
  * the messages are all-gathered after the vertex kernel (grouped
  * ncclBroadcast). Set the same value on every rank before a run. */
 gg_status gg_exchange_set_fused(gg_exchange* x, int on);
+/* Transport health check (collective: every rank calls it). Over NCCL it
+ * all-gathers ragged rank slices with the engine's grouped ncclBroadcast,
+ * sum- and max-all-reduces rank vectors and compares the results with their
+ * closed forms; GG_NCCL with a message on any difference. A one-rank
+ * communicator is valid (runs the same calls). No-op for the in-process
+ * transport. */
+gg_status gg_exchange_selftest(gg_exchange* x, gg_error* err);
 gg_status gg_exchange_destroy(gg_exchange* x);
 
 /* Host metrics (metrics.cpp:60-113); accuracy = (1 - err) * 100. */

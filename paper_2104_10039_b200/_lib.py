@@ -21,7 +21,7 @@ EXPORTS = (
     "gg_dev_graph_info", "gg_dev_graph_create_rmat", "gg_dev_graph_export", "gg_bp_priors",
     "gg_run_pr", "gg_run_sssp", "gg_run_wcc", "gg_run_bp", "gg_validate", "gg_mode_for",
     "gg_select_superstep_iterations", "gg_sparsify", "gg_partition_plan", "gg_nccl_unique_id",
-    "gg_exchange_nccl_create", "gg_exchange_local_group", "gg_exchange_destroy", "gg_exchange_set_fused", "gg_topk_error", "gg_relative_error",
+    "gg_exchange_nccl_create", "gg_exchange_local_group", "gg_exchange_destroy", "gg_exchange_set_fused", "gg_exchange_selftest", "gg_topk_error", "gg_relative_error",
     "gg_stretch_error", "gg_dev_graph_symmetrized",
 )
 
@@ -148,6 +148,7 @@ def lib():
     L.gg_nccl_unique_id.argtypes = [vp]
     L.gg_exchange_nccl_create.argtypes = [vp, C.c_int, C.c_int, P(vp), P(ErrorC)]
     L.gg_exchange_destroy.argtypes = [vp]
+    L.gg_exchange_selftest.argtypes = [vp, P(ErrorC)]
     if hasattr(L, "gg_exchange_set_fused"):
         L.gg_exchange_set_fused.argtypes = [vp, C.c_int]
     L.gg_exchange_local_group.argtypes = [C.c_int, P(vp)]

@@ -432,6 +432,65 @@ gg_status gg_exchange_set_fused(gg_exchange* x, int on) {
     });
 }
 
+// Transport health check. Every rank fills its own slice of a small buffer
+// with a rank pattern, the slices are all-gathered with the grouped
+// ncclBroadcast of exchange_slices (ragged slice lengths, rank r owns
+// 1000 + 37 r words), a rank vector is sum-all-reduced and the one-word
+// barrier all-reduce is issued, all on one private stream; the results are
+// read back and compared with the closed forms.
+gg_status gg_exchange_selftest(gg_exchange* x, gg_error* err) {
+    return ggb::guarded(err, [&] {
+        if (!x) throw ggb::Error(GG_INVALID_ARGUMENT, "null exchange");
+        if (x->local) return;  // host barriers + device copies: covered by the engine runs
+        if (!x->comm) throw ggb::Error(GG_NCCL, "exchange without communicator");
+        const ggb::NcclApi& api = ggb::nccl();
+        const int R = x->nranks, me = x->rank;
+        std::vector<uint64_t> base(R + 1, 0);
+        for (int r = 0; r < R; ++r) base[r + 1] = base[r] + 1000 + 37 * (uint64_t)r;
+        const uint64_t total = base[R], nred = 4096;
+        auto pat = [](int r, uint64_t i) { return (uint32_t)(0x9E3779B9u * (uint32_t)(r + 1) + (uint32_t)i); };
+        std::vector<uint32_t> h(total + nred + 1, 0);
+        for (uint64_t i = base[me]; i < base[me + 1]; ++i) h[i] = pat(me, i);
+        for (uint64_t i = 0; i < nred; ++i) h[total + i] = (uint32_t)(me + 1) * (uint32_t)(i + 1);
+        h[total + nred] = (uint32_t)me;
+        cudaStream_t st = nullptr;
+        uint32_t* d = nullptr;
+        GGB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        GGB_CUDA(cudaMalloc(&d, h.size() * 4));
+        try {
+            GGB_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+            ggb::nccl_check(api.GroupStart(), "ncclGroupStart");
+            for (int r = 0; r < R; ++r)
+                ggb::nccl_check(api.Broadcast(d + base[r], d + base[r], (base[r + 1] - base[r]) * 4,
+                                              ncclChar, r, x->comm, st), "ncclBroadcast(selftest)");
+            ggb::nccl_check(api.GroupEnd(), "ncclGroupEnd");
+            ggb::nccl_check(api.AllReduce(d + total, d + total, nred, ncclUint32, ncclSum, x->comm, st),
+                            "ncclAllReduce(selftest sum)");
+            ggb::nccl_check(api.AllReduce(d + total + nred, d + total + nred, 1, ncclUint32, ncclMax,
+                                          x->comm, st), "ncclAllReduce(selftest max)");
+            GGB_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost, st));
+            GGB_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaFree(d);
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaFree(d);
+        cudaStreamDestroy(st);
+        for (int r = 0; r < R; ++r)
+            for (uint64_t i = base[r]; i < base[r + 1]; ++i)
+                if (h[i] != pat(r, i))
+                    throw ggb::Error(GG_NCCL, "exchange selftest: gathered slice of rank " +
+                                                  std::to_string(r) + " differs");
+        const uint32_t tri = (uint32_t)((uint64_t)R * (R + 1) / 2);
+        for (uint64_t i = 0; i < nred; ++i)
+            if (h[total + i] != tri * (uint32_t)(i + 1))
+                throw ggb::Error(GG_NCCL, "exchange selftest: all-reduce sum differs");
+        if (h[total + nred] != (uint32_t)(R - 1))
+            throw ggb::Error(GG_NCCL, "exchange selftest: all-reduce max differs");
+    });
+}
+
 gg_status gg_exchange_destroy(gg_exchange* x) {
     return ggb::guarded(nullptr, [&] {
         if (!x) return;

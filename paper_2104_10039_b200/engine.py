@@ -577,6 +577,13 @@ class Exchange:
         after it. Same value on every rank (gg_exchange_set_fused)."""
         _raise(L.lib().gg_exchange_set_fused(self.handle, 1 if on else 0), None)
 
+    def selftest(self) -> None:
+        """Collective transport check (gg_exchange_selftest): ragged all-gather
+        and all-reduces over the communicator against their closed forms;
+        raises on any difference. Every rank calls it."""
+        err = L.ErrorC()
+        _raise(L.lib().gg_exchange_selftest(self.handle, C.byref(err)), err)
+
     @staticmethod
     def unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()

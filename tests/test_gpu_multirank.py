@@ -205,3 +205,24 @@ def test_ranks_agree_on_the_exchange_path(ggb):
     for rep in out:
         assert not rep.exchange_fused
         _same(rep, single)
+
+
+def test_nccl_transport_selftest_one_rank_communicator(ggb):
+    """The NCCL transport's own calls on this GPU: ncclGetUniqueId,
+    ncclCommInitRank, the grouped ncclBroadcast all-gather, the sum and max
+    all-reduces and ncclCommDestroy run over a one-rank communicator and are
+    compared with their closed forms (gg_exchange_selftest). bench.py runs
+    the same check on every rank before a multi-GPU measurement."""
+    x = ggb.Exchange(0, 1, ggb.Exchange.unique_id())
+    try:
+        x.selftest()
+        x.selftest()  # a second round on the same communicator
+    finally:
+        x.close()
+
+
+def test_local_transport_selftest_is_a_noop(ggb):
+    xs = ggb.Exchange.local_group(2)
+    for x in xs:
+        x.selftest()
+        x.close()
