@@ -492,10 +492,12 @@ def ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": DTYPE[wl["prog"]], "data": "synthetic R-MAT (seeded, built on device)",
-        "config": config_json(args, wl, world) | {"vertices": n, "edges": e,
-                                                 "max_iterations": budget,
-                                                 "iterations_per_step": reps[0].iterations_run,
-                                                 "edges_per_step": reps[0].total_processed_edges},
+        # config is the workload only and identical on both arms; the shape of a
+        # step (which differs: a whole gg run here, a bounded sample there) is "step"
+        "config": config_json(args, wl, world) | {"vertices": n, "edges": e},
+        "step": {"what": "one whole gg run (sparsify, every iteration, early exit)",
+                 "max_iterations": budget, "iterations_per_step": reps[0].iterations_run,
+                 "edges_per_step": reps[0].total_processed_edges},
         "gteps_sparsified_kernel": round(g_sp, 3) if g_sp else None,
         "gteps_full_kernel": round(g_full, 3) if g_full else None,
         "accuracy": accuracy,
@@ -796,6 +798,8 @@ def reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": DTYPE[wl["prog"]],
         "data": "synthetic R-MAT (seeded, CPU generator)",
         "config": config_json(args, wl, world) | {"vertices": g.n, "edges": g.e},
+        "step": {"what": "bounded sample: the first (approximate) iteration of the gg run",
+                 "max_iterations": STEP_ITERS, "iterations_per_step": STEP_ITERS},
         "accuracy": acc,
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
