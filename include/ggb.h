@@ -250,8 +250,9 @@ gg_status gg_exchange_set_fused(gg_exchange* x, int on);
  * all-gathers ragged rank slices with the engine's grouped ncclBroadcast,
  * sum- and max-all-reduces rank vectors and compares the results with their
  * closed forms; GG_NCCL with a message on any difference. A one-rank
- * communicator is valid (runs the same calls). No-op for the in-process
- * transport. */
+ * communicator is valid (runs the same calls). Call it with the
+ * communicator's device current (the one current at gg_exchange_nccl_create).
+ * No-op for the in-process transport. */
 gg_status gg_exchange_selftest(gg_exchange* x, gg_error* err);
 gg_status gg_exchange_destroy(gg_exchange* x);
 
