@@ -324,7 +324,7 @@ __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __r
         for (int k = 0; k < kW; ++k) {
             if ((word[k] >> lane) & 1u) {
                 const uint64_t pos = out_pad + base[k] + (uint64_t)__popc(word[k] & lt);
-                s_src[pos] = sv[k];
+                s_src[sp_slot(pos)] = sv[k];
                 if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[k];
             }
         }
@@ -494,7 +494,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 const uint32_t ok = __shfl_sync(0xffffffffu, off[kw / 32], kw % 32);
                 if ((wk >> lane) & 1u) {
                     const uint64_t pos = wbase + ok + (uint32_t)__popc(wk & lt);
-                    s_src[pos] = sv[b % D][k];
+                    s_src[sp_slot(pos)] = sv[b % D][k];
                     if constexpr (WB > 0) static_cast<WT*>(s_w)[pos] = wv[b % D][k];
                 }
             }
@@ -697,7 +697,7 @@ void presparse_chunk(DevGraph& g, const SparsifySpec& h, uint64_t e_lo, uint64_t
     const uint64_t nwords = (g.e_loc + 31) / 32;
     uint32_t* bitmap = g.ws.get<uint32_t>("bitmap", nwords + 1);
     uint64_t* wpref = g.ws.get<uint64_t>("rb.wpref", nwords + 1);
-    uint32_t* s_src = g.ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
+    uint32_t* s_src = g.ws.get<uint32_t>("s_src", g.e_loc + 2 * kChunkEdges + kRun);
     const size_t wsz = weight_size(g.wkind);
     void* s_w = wsz ? g.ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
     const uint64_t te = presparse_tile_edges();

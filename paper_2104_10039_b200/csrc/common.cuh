@@ -24,6 +24,21 @@ constexpr int kMaxPeers = 8;
 constexpr int kWarp = 32;
 constexpr int kRun = 16;                 // consecutive in-edges folded by one lane
 constexpr int kChunkEdges = kWarp * kRun;  // in-edges per warp task (512)
+
+// Storage order of a SPARSIFIED list's sources (written only by the
+// compaction kernels, read only by the approximate gather): inside every
+// aligned task block of 512 positions the 4-source quads are transposed, quad
+// q of lane L's run lies at quad q * 32 + L. A lane's four 128-bit source
+// loads then touch 4 x 512 contiguous bytes per warp instead of 16 lines at a
+// 64-byte lane stride each (4x fewer L1TEX wavefronts on the source stream).
+// The full list keeps position order (compaction, export and the loaders
+// index it by edge).
+static_assert(kRun == 16 && kWarp == 32, "sp_slot assumes 16-position runs in 512-position tasks");
+__host__ __device__ __forceinline__ uint64_t sp_slot(uint64_t p) {
+    return (p & ~511ull) | (((p >> 2) & 3ull) << 7) | (((p >> 4) & 31ull) << 2) | (p & 3ull);
+}
+// uint4 index (inside the task block) of quad i of lane L's run
+__host__ __device__ __forceinline__ int sp_quad(int L, int i) { return i * 32 + L; }
 constexpr int kBlockThreads = 128;       // edge kernels: 4 warps per CTA
 constexpr int kWarpsPerBlock = kBlockThreads / kWarp;
 

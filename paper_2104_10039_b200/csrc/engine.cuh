@@ -244,7 +244,7 @@ struct Engine {
         if (sparse) {  // engine.hpp:151-161
             bitmap = ws.get<uint32_t>("bitmap", nwords + 1);
             s_off = ws.get<uint64_t>("s_off", R + 1);
-            s_src = ws.get<uint32_t>("s_src", g.e_loc + kChunkEdges + kRun);
+            s_src = ws.get<uint32_t>("s_src", g.e_loc + 2 * kChunkEdges + kRun);
             s_w = wsz ? ws.get("s_w", (g.e_loc + kChunkEdges + kRun) * wsz) : nullptr;
             if (g.pre_sparse && g.pre_sigma == cfg.sigma && g.pre_seed == cfg.seed) {
                 kept = presparse_finish(g, s_off, sp);  // sparsified during the upload
@@ -308,6 +308,7 @@ struct Engine {
             EdgeArgs<P, W> ea{};
             ea.prog = prog;
             ea.src = approx ? s_src : g.src;
+            ea.src_quads = approx;  // the compaction writes sp_slot order
             ea.w = static_cast<const W*>(approx ? s_w : g.w);
             ea.run_i = L.run_i;
             ea.nz_row = approx ? L.nz_vid : nullptr;  // the full list's rows are its nz indices

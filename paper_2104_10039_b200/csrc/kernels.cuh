@@ -91,7 +91,8 @@ constexpr int kStageStarts = kChunkEdges + 2;
 template <class P, class W>
 struct EdgeArgs {
     P prog;
-    const uint32_t* __restrict__ src;       // [padded position]
+    const uint32_t* __restrict__ src;       // [padded position]; sparsified list: [sp_slot(position)]
+    bool src_quads;                         // src is in sp_slot order (common.cuh)
     const W* __restrict__ w;                // [padded position]
     const uint32_t* __restrict__ run_i;     // [run] non-empty vertex at its first position
     const uint32_t* __restrict__ nz_row;    // [nz] row of the list's i-th non-empty vertex
@@ -203,7 +204,9 @@ struct HotTable {
     uint32_t n = 0;     // slots [0, n) are in shared memory
 };
 
-template <class P, class W, bool HOT = false>
+// SQ: the list may be a sparsified one in sp_slot order (a.src_quads); false
+// for the superstep kernels, which only ever walk the full list.
+template <class P, class W, bool HOT = false, bool SQ = true>
 __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, uint64_t lo,
                                          uint64_t hi, typename P::Message (&m)[kRun],
                                          WStore<W> (&wr)[kRun], uint64_t pol_stream,
@@ -211,19 +214,24 @@ __device__ __forceinline__ void load_run(const EdgeArgs<P, W>& a, uint64_t P0, u
                                          HotTable ht = {}) {
     uint32_t s[kRun];
     if (lo == P0 && hi == P0 + kRun) {
-        const uint4* sp = reinterpret_cast<const uint4*>(a.src + P0);
+        // sp_slot order: quad i of this lane's run at quad i * 32 + lane of the task block
+        const bool quads = SQ && a.src_quads;
+        const int L = (int)((P0 >> 4) & 31ull);
+        const uint4* sp = quads ? reinterpret_cast<const uint4*>(a.src + (P0 & ~511ull))
+                                : reinterpret_cast<const uint4*>(a.src + P0);
 #pragma unroll
         for (int i = 0; i < kRun / 4; ++i) {
             uint4 q;
             asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                         : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(sp + i), "l"(pol_stream));
+                         : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(sp + (quads ? sp_quad(L, i) : i)), "l"(pol_stream));
             s[4 * i] = q.x; s[4 * i + 1] = q.y; s[4 * i + 2] = q.z; s[4 * i + 3] = q.w;
         }
     } else {
 #pragma unroll
         for (int j = 0; j < kRun; ++j) {
             const uint64_t p = P0 + j;
-            s[j] = (p >= lo && p < hi) ? ld_stream_u32(a.src + p, pol_stream) : 0u;
+            s[j] = (p >= lo && p < hi)
+                       ? ld_stream_u32(a.src + (SQ && a.src_quads ? sp_slot(p) : p), pol_stream) : 0u;
         }
     }
     // Every gather is issued unconditionally and independently (positions
@@ -451,7 +459,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
             ri = a.run_i[r];
-            load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
+            load_run<P, W, HOT, MODE == kEdgePlain>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
     const uint32_t cnt = i_next - i0 + 2;  // <= kStageStarts
@@ -469,7 +477,7 @@ __device__ __forceinline__ void edge_task(const EdgeArgs<P, W>& a, int16_t* st0,
         len = hi > lo ? (int)(hi - lo) : 0;
         if (len > 0) {
             ri = a.run_i[r];
-            load_run<P, W, HOT>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
+            load_run<P, W, HOT, MODE == kEdgePlain>(a, P0, lo, hi, m, wr, pol_stream, pol_hot, pol_cold, ht);
         }
     }
     const int rlo = (int)(lo - tstart), rhi = (int)(hi - tstart);  // task-relative

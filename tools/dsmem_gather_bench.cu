@@ -10,6 +10,10 @@
 //                 the rest through ld.global.nc
 //           lds   slots < T from the CTA's own table, the rest ld.global.nc
 //           skip  slots < cluster * T not gathered at all (the bound)
+//           ldgc / pol2c   as ldg / pol2, but the index stream is read
+//                 COALESCED (lane l takes quad q*32 + l instead of the four
+//                 quads of its own 16-index run): what the engine's
+//                 lane-contiguous runs cost in L1TEX wavefronts
 //
 // Index stream: the hot-first slot marginal of an R-MAT s26 source (same
 // emulation as tma_gather_bench.cu). Messages: f64[2^26].
@@ -69,7 +73,8 @@ __global__ void count_hot(const uint32_t* idx, uint64_t m, uint32_t h, unsigned 
 
 enum { kLdg = 0, kDsm = 1, kLds = 2, kSkip = 3, kPol2 = 4, kPol1 = 5, kWin = 6 };
 
-template <int MODE>
+
+template <int MODE, bool COAL = false>
 __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double* __restrict__ x,
                       int tlog, int clog, double* __restrict__ out) {
     extern __shared__ __align__(16) double tab[];
@@ -106,15 +111,16 @@ __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double
     double acc = 0.0;
     for (uint64_t c = gw; c < m / 512; c += nw) {
         uint32_t s[16];
-        const uint4* ip = reinterpret_cast<const uint4*>(idx + c * 512) + lane * 4;
+        const uint4* ip = reinterpret_cast<const uint4*>(idx + c * 512) + (COAL ? lane : lane * 4);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             uint4 v;
+            const uint4* iq = ip + (COAL ? q * 32 : q);
             if (MODE >= kPol2)
                 asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ip + q), "l"(pol_stream));
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(iq), "l"(pol_stream));
             else
-                v = __ldg(ip + q);
+                v = __ldg(iq);
             s[4 * q] = v.x; s[4 * q + 1] = v.y; s[4 * q + 2] = v.z; s[4 * q + 3] = v.w;
         }
         double v[16];
@@ -156,12 +162,12 @@ __global__ void bench(const uint32_t* __restrict__ idx, uint64_t m, const double
     if (acc == 1.2345) out[0] = acc;
 }
 
-template <int MODE>
+template <int MODE, bool COAL = false>
 static void run(const char* name, int clog, int tlog, int reps, int threads, const uint32_t* idx, uint64_t m,
                 const double* x, double* out, unsigned long long* cnt) {
     const int C = 1 << clog;
     const size_t smem = (MODE == kDsm || MODE == kLds) ? (size_t)8 << tlog : 0;
-    auto k = bench<MODE>;
+    auto k = bench<MODE, COAL>;
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (MODE == kDsm && C > 8) CK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int sms = 0;
@@ -246,6 +252,8 @@ int main(int argc, char** argv) {
     else if (mode == "lds") run<kLds>("lds", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else if (mode == "pol2") run<kPol2>("pol2", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else if (mode == "pol1") run<kPol1>("pol1", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "ldgc") run<kLdg, true>("ldgc", clog, tlog, reps, threads, idx, m, x, out, cnt);
+    else if (mode == "pol2c") run<kPol2, true>("pol2c", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else if (mode == "win") run<kWin>("win", clog, tlog, reps, threads, idx, m, x, out, cnt);
     else run<kSkip>("skip", clog, tlog, reps, threads, idx, m, x, out, cnt);
     return 0;
