@@ -298,7 +298,7 @@ template <int WB>
 __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w,
                                uint64_t e_loc, uint64_t in_pad, const uint32_t* __restrict__ bitmap,
                                const uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
-                               void* __restrict__ s_w, uint64_t out_pad) {
+                               void* __restrict__ s_w, uint64_t out_pad, bool quads) {
     using WT = std::conditional_t<WB == 8, unsigned long long, uint32_t>;
     constexpr int kW = 8;
     const int lane = threadIdx.x & 31;
@@ -324,7 +324,7 @@ __global__ void compact_kernel(const uint32_t* __restrict__ src, const void* __r
         for (int k = 0; k < kW; ++k) {
             if ((word[k] >> lane) & 1u) {
                 const uint64_t pos = out_pad + base[k] + (uint64_t)__popc(word[k] & lt);
-                s_src[sp_slot(pos)] = sv[k];
+                s_src[quads ? sp_slot(pos) : pos] = sv[k];
                 if constexpr (WB != 0) static_cast<WT*>(s_w)[pos] = wv[k];
             }
         }
@@ -389,7 +389,8 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                     uint64_t in_pad, uint32_t* __restrict__ bitmap, uint64_t nwords, uint64_t e_base,
                     SparsifySpec h, uint64_t* __restrict__ wpref, uint32_t* __restrict__ s_src,
                     void* __restrict__ s_w, unsigned long long* __restrict__ tstate,
-                    uint32_t* __restrict__ ticket, uint64_t tile_base, uint64_t ntiles) {
+                    uint32_t* __restrict__ ticket, uint64_t tile_base, uint64_t ntiles,
+                    bool quads) {
     using WT = std::conditional_t<WB == 8, unsigned long long, uint32_t>;
     constexpr int kWarps = kScanThreads / 32;
     __shared__ uint32_t s_tile;
@@ -494,7 +495,7 @@ scan_compact_kernel(const uint32_t* __restrict__ src, const void* __restrict__ w
                 const uint32_t ok = __shfl_sync(0xffffffffu, off[kw / 32], kw % 32);
                 if ((wk >> lane) & 1u) {
                     const uint64_t pos = wbase + ok + (uint32_t)__popc(wk & lt);
-                    s_src[sp_slot(pos)] = sv[b % D][k];
+                    s_src[quads ? sp_slot(pos) : pos] = sv[b % D][k];
                     if constexpr (WB > 0) static_cast<WT*>(s_w)[pos] = wv[b % D][k];
                 }
             }
@@ -532,19 +533,19 @@ static void launch_scan_compact(DevGraph& g, uint32_t* bitmap, const SparsifySpe
     if (scan_only)
         scan_compact_kernel<-1, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, tile_lo, tile_hi);
+            ticket, tile_lo, tile_hi, sp_quads(g));
     else if (wb == 0)
         scan_compact_kernel<0, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, tile_lo, tile_hi);
+            ticket, tile_lo, tile_hi, sp_quads(g));
     else if (wb == 4)
         scan_compact_kernel<4, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, tile_lo, tile_hi);
+            ticket, tile_lo, tile_hi, sp_quads(g));
     else
         scan_compact_kernel<8, HASH><<<gr, kScanThreads, 0, g.stream>>>(
             g.src, g.w, g.e_loc, g.full.pad, bitmap, nwords, g.e_base, h, wpref, s_src, s_w, tstate,
-            ticket, tile_lo, tile_hi);
+            ticket, tile_lo, tile_hi, sp_quads(g));
     GGB_CUDA(cudaGetLastError());
 }
 
@@ -754,13 +755,13 @@ uint64_t rebuild_sparse(DevGraph& g, uint32_t* bitmap, uint64_t* s_off, uint32_t
     if (g.e_loc) {
         if (wb == 0)
             compact_kernel<0><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
-                                                        wpref, s_src, s_w, pad);
+                                                        wpref, s_src, s_w, pad, sp_quads(g));
         else if (wb == 4)
             compact_kernel<4><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
-                                                        wpref, s_src, s_w, pad);
+                                                        wpref, s_src, s_w, pad, sp_quads(g));
         else
             compact_kernel<8><<<gr, 256, 0, g.stream>>>(g.src, g.w, g.e_loc, g.full.pad, bitmap,
-                                                        wpref, s_src, s_w, pad);
+                                                        wpref, s_src, s_w, pad, sp_quads(g));
         GGB_CUDA(cudaGetLastError());
     }
     build_sparse_layout(g, bitmap, wpref, s_off, pad, kept, meta);

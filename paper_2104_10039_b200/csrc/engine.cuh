@@ -308,7 +308,7 @@ struct Engine {
             EdgeArgs<P, W> ea{};
             ea.prog = prog;
             ea.src = approx ? s_src : g.src;
-            ea.src_quads = approx;  // the compaction writes sp_slot order
+            ea.src_quads = approx && sp_quads(g);  // as the compaction wrote it
             ea.w = static_cast<const W*>(approx ? s_w : g.w);
             ea.run_i = L.run_i;
             ea.nz_row = approx ? L.nz_vid : nullptr;  // the full list's rows are its nz indices

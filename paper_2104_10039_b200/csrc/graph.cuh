@@ -175,6 +175,14 @@ struct DevGraph {
 };
 
 size_t weight_size(gg_weight_kind k);
+// A graph's sparsified sources are stored in sp_slot order (common.cuh) iff
+// it carries no weights: a graph-level rule, so the upload-overlapped
+// sparsification, every rebuild and the approximate gather agree without
+// knowing the program. Measured (profiles/r2_summary.md, session 5): the
+// coalesced source loads pay on the unweighted configs (c5 gathers -3.2 %,
+// c3 +1 % GTEPS); on weighted graphs the dearer compaction stores outweigh
+// them (c4 -2.5 %, c2 -0.4 %).
+inline bool sp_quads(const DevGraph& g) { return weight_size(g.wkind) == 0; }
 // graph creation steps shared by the C-ABI constructors (capi.cu)
 void setup_common(DevGraph& g, const gg_part_opts* opts);
 void finish_graph(DevGraph& g, const uint64_t* host_off_full);
